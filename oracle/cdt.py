@@ -1,0 +1,22 @@
+"""Oracle-side CDT table for the discrete Gaussian (TEST INFRASTRUCTURE).
+
+sigma = 3.2, support [-T, T] with T = floor(6 sigma) = 19
+(reading G17 in DESIGN.md).  Thresholds thr[k] = floor(2^64 * CDF(-T + k)) for
+k = 0 .. 2T-1, computed with Python's decimal module at 60 significant digits.
+The CUDA library computes its own table independently (long double); the two
+are compared by tests/test_keygen_parity.py.
+"""
+from decimal import Decimal, getcontext
+
+
+def cdt_table(sigma: float = 3.2, T: int = 19):
+    getcontext().prec = 60
+    s = Decimal(str(sigma))
+    rho = [(-(Decimal(e) ** 2) / (2 * s * s)).exp() for e in range(-T, T + 1)]
+    Z = sum(rho)
+    out, acc = [], Decimal(0)
+    two64 = Decimal(2) ** 64
+    for k in range(2 * T):
+        acc += rho[k]
+        out.append(int((acc / Z * two64).to_integral_value(rounding="ROUND_FLOOR")))
+    return out

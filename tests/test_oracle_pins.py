@@ -1,0 +1,429 @@
+"""Pins for the CPU oracle (oracle/), independent of the oracle's own formulas.
+
+Each test checks the oracle against something the paper or mathematics fixes:
+library routines it does not use (numpy Philox, Python big-int convolution,
+fractions), closed forms, evaluation homomorphisms, the SPEC.md worked values,
+and the noiseless message laws of the lemmas.  Citations are PAPER.md lines.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import synth
+from oracle.cdt import cdt_table
+from oracle.oracle import Oracle, philox
+
+
+# ----------------------------------------------------------------------------- helpers
+def negacyclic_bigint(a, b, N, Q):
+    """Exact negacyclic product via Python integers and numpy's object convolution."""
+    full = np.convolve(np.array([int(x) for x in a], dtype=object), np.array([int(x) for x in b], dtype=object))
+    out = [0] * N
+    for k, v in enumerate(full):
+        if k < N:
+            out[k] += v
+        else:
+            out[k - N] -= v
+    return np.array([x % Q for x in out], dtype=np.uint64)
+
+
+def psi_2n(N, Q):
+    """A primitive 2N-th root of unity mod Q (Q = 1 mod 2N)."""
+    for g in range(2, 1000):
+        psi = pow(g, (Q - 1) // (2 * N), Q)
+        if pow(psi, N, Q) == Q - 1:
+            return psi
+    raise AssertionError
+
+
+def evalp(a, x, Q):
+    r = 0
+    for c in reversed([int(v) for v in a]):
+        r = (r * x + c) % Q
+    return r
+
+
+def centered(v, Q):
+    v = int(v) % Q
+    return v - Q if v > Q // 2 else v
+
+
+# ----------------------------------------------------------------------------- PRNG / CDT
+@pytest.mark.parametrize("key", [(0, 0), (5, 7), (2**64 - 1, 12345)])
+@pytest.mark.parametrize("ctr", [(1, 0, 0, 0), (7, 3, 9, 2), (2**40, 1, 0, 5)])
+def test_philox4x64_matches_numpy(key, ctr):
+    # numpy's Philox (4x64-10) increments its counter before each block, so its
+    # first block for state counter c is our block for counter c+1.
+    g = np.random.Philox(key=np.array(key, dtype=np.uint64),
+                         counter=np.array([ctr[0] - 1, ctr[1], ctr[2], ctr[3]], dtype=np.uint64))
+    ref = g.random_raw(4).astype(np.uint64)
+    assert np.array_equal(philox(ctr, key), ref)
+
+
+def test_cdt_table_matches_float_gaussian():
+    thr = cdt_table()
+    T = len(thr) // 2
+    assert T == 19 and all(a < b for a, b in zip(thr, thr[1:]))
+    rho = [math.exp(-e * e / (2 * 3.2 ** 2)) for e in range(-T, T + 1)]
+    Z = sum(rho)
+    acc = 0.0
+    for k in range(2 * T):
+        acc += rho[k] / Z
+        assert abs(thr[k] / 2**64 - acc) < 1e-12
+    for k in range(T):  # symmetry of the centred Gaussian
+        assert abs(thr[k] + thr[2 * T - 1 - k] - 2**64) < 2**12
+
+
+def test_encryption_error_variance_and_bound(toy_cfg):
+    cfg = synth.load_config("tiny")
+    o = Oracle(cfg)
+    s, S = o.keygen_secrets(1)
+    cts = o.rlwe_encrypt(99, S, np.zeros((64, o.N), dtype=np.uint64))
+    errs = np.array([centered(v, o.Q) for c in cts for v in o.rlwe_phase(S, c)])
+    assert np.abs(errs).max() <= 19
+    assert abs(errs.var() - 3.2 ** 2) < 0.1 * 3.2 ** 2          # SPEC.md:74 style check
+    assert abs(errs.mean()) < 0.1
+
+
+def test_secret_distributions():
+    o = Oracle(synth.load_config("large"))
+    s, S = o.keygen_secrets(3)
+    assert set(np.unique(s)) <= {-1, 0, 1} and set(np.unique(S)) <= {-1, 0, 1}
+    for v in (-1, 0, 1):
+        assert abs((S == v).mean() - 1 / 3) < 0.05
+    ob = Oracle(synth.load_config("tiny"))
+    sb, _ = ob.keygen_secrets(3)
+    assert set(np.unique(sb)) <= {0, 1} and 0.3 < sb.mean() < 0.7
+
+
+# ----------------------------------------------------------------------------- ring
+def test_ring_spec_example():
+    o = Oracle(synth.load_config("tiny"))
+    N, Q = o.N, o.Q
+    a = np.zeros(N, np.uint64); a[N - 1] = 1
+    b = np.zeros(N, np.uint64); b[1] = 1
+    c = o.ring_mul(a, b)                                   # X^{N-1} * X = -1
+    assert c[0] == Q - 1 and not c[1:].any()
+
+
+@pytest.mark.parametrize("name", ["toy", "tiny", "large"])
+def test_ring_mul_vs_bigint_and_evaluation(name, toy_cfg):
+    cfg = toy_cfg if name == "toy" else synth.load_config(name)
+    o = Oracle(cfg)
+    N, Q = o.N, o.Q
+    rng = np.random.default_rng(1)
+    a = rng.integers(0, Q, N, dtype=np.uint64)
+    b = rng.integers(0, Q, N, dtype=np.uint64)
+    c = o.ring_mul(a, b)
+    if N <= 256:
+        assert np.array_equal(c, negacyclic_bigint(a, b, N, Q))
+    psi = psi_2n(N, Q)
+    for k in (1, 3, 2 * N - 1):                             # a(w) b(w) = c(w) at roots of X^N+1
+        w = pow(psi, k, Q)
+        assert evalp(c, w, Q) == evalp(a, w, Q) * evalp(b, w, Q) % Q
+
+
+def test_ring_mul_overflow_canary():
+    o = Oracle(synth.load_config("large"))
+    N, Q = o.N, o.Q
+    a = np.full(N, Q - 1, np.uint64)
+    c = o.ring_mul(a, a)
+    # (-1)(-1) * sum_{i+j=k} 1 - sum_{i+j=k+N} 1 = (k+1) - (N-1-k)
+    exp = np.array([((k + 1) - (N - 1 - k)) % Q for k in range(N)], dtype=np.uint64)
+    assert np.array_equal(c, exp)
+
+
+def test_monomial_mul_matches_ring_mul(toy_cfg):
+    o = Oracle(toy_cfg)
+    N, Q = o.N, o.Q
+    a = np.random.default_rng(2).integers(0, Q, N, dtype=np.uint64)
+    for e in range(-2 * N, 4 * N):
+        E = e % (2 * N)
+        mono = np.zeros(N, np.uint64)
+        mono[E % N] = 1 if E < N else Q - 1
+        assert np.array_equal(o.monomial_mul(a, e), o.ring_mul(mono, a))
+
+
+# ----------------------------------------------------------------------------- Decomp / ModSwitch
+def test_decomp_spec_example_and_recomposition():
+    o = Oracle(synth.load_config("tiny"))
+    assert list(o.decomp(27, 2, 4)) == [3, 2, 1, 0]          # SPEC.md:115 (q=256, L=4)
+    for x in range(0, 4096, 7):
+        d = o.decomp(x, 3, 4)
+        assert all(v < 8 for v in d) and sum(int(v) * 8**r for r, v in enumerate(d)) == x
+    rng = np.random.default_rng(3)
+    Q = 18014398509404161
+    for x in rng.integers(0, Q, 200, dtype=np.uint64):
+        d = o.decomp(int(x), 14, 4)
+        assert sum(int(v) << (14 * r) for r, v in enumerate(d)) == int(x)
+
+
+def test_mod_switch_spec_and_exact_rounding():
+    o = Oracle(synth.load_config("tiny"))
+    assert o.mod_switch(8192, 2**14, 2**11) == 1024
+    for Qf, qt in [(97, 32), (12289, 512), (2**32, 512), (134215681, 2**32)]:
+        for x in list(range(0, min(Qf, 3000))) + [Qf - 1]:
+            r = Fraction(qt * x, Qf)
+            exp = math.floor(r + Fraction(1, 2)) % qt          # round half up
+            assert o.mod_switch(x, Qf, qt) == exp
+
+
+# ----------------------------------------------------------------------------- SampleExt (F1)
+@pytest.mark.parametrize("name", ["toy", "tiny"])
+def test_sample_extract_phase_identity_all_k(name, toy_cfg):
+    cfg = toy_cfg if name == "toy" else synth.load_config(name)
+    o = Oracle(cfg)
+    s, S = o.keygen_secrets(5)
+    msg = np.random.default_rng(4).integers(0, o.Q, o.N, dtype=np.uint64)
+    ct = o.rlwe_encrypt(6, S, msg)[0]
+    ph = o.rlwe_phase(S, ct)                                 # noisy phase, exact integers
+    for k in range(1, o.N + 1):
+        lwe = o.sample_extract(ct, k)
+        assert o.lwe_phase_q(S, lwe) == int(ph[k - 1])       # Lemma 2002 / proof 3264-3274
+
+
+def test_sample_extract_cases_display_reading_fails(toy_cfg):
+    """F1: with NSgn(0) = +1 (the cases display at PAPER.md:2956) the identity breaks."""
+    o = Oracle(toy_cfg)
+    s, S = o.keygen_secrets(5)
+    ct = o.rlwe_encrypt(6, S, np.arange(o.N, dtype=np.uint64))[0]
+    ph = o.rlwe_phase(S, ct)
+    k = 3
+    lwe = o.sample_extract(ct, k)
+    alt = lwe.copy()
+    alt[1 + k] = (o.Q - int(alt[1 + k])) % o.Q              # i = k+1: x = k-i+1 = 0 flips sign
+    assert o.lwe_phase_q(S, alt) != int(ph[k - 1]) or S[(k + 1 - 1)] == 0
+
+
+# ----------------------------------------------------------------------------- extProd / CMux / BR
+@pytest.fixture
+def toy_noiseless(toy_cfg):
+    o = Oracle(toy_cfg, noiseless=True)
+    K = o.keys(21)
+    return o, K
+
+
+def test_ext_prod_and_cmux_message_law(toy_noiseless):
+    o, K = toy_noiseless
+    rng = np.random.default_rng(7)
+    g = o.rlwe_encrypt(31, K["S"], rng.integers(0, o.Q, o.N, dtype=np.uint64))[0]
+    h = o.rlwe_encrypt(32, K["S"], rng.integers(0, o.Q, o.N, dtype=np.uint64))[0]
+    pg, ph = o.rlwe_phase(K["S"], g), o.rlwe_phase(K["S"], h)
+    for i in range(o.n):
+        Cm = K["brk"][i, 0]                                   # RGSW(s[i]) (binary u=[1])
+        bit = int(K["s"][i])
+        ep = o.ext_prod(Cm, g)
+        assert np.array_equal(o.rlwe_phase(K["S"], ep), (pg * bit) % o.Q)
+        cm = o.cmux(Cm, g, h)
+        assert np.array_equal(o.rlwe_phase(K["S"], cm), pg if bit else ph)
+
+
+def test_blind_rotate_message_law(toy_noiseless):
+    o, K = toy_noiseless
+    rng = np.random.default_rng(8)
+    m = rng.integers(0, o.Q, o.N, dtype=np.uint64)
+    acc = np.zeros((2, o.N), np.uint64)
+    acc[0] = m                                                # trivial RLWE [m, 0]
+    cases = [np.zeros(o.n, np.uint32)] + [rng.integers(0, 2 * o.N, o.n).astype(np.uint32) for _ in range(40)]
+    for i in range(o.n):
+        for v in (1, o.N - 1, o.N, 2 * o.N - 1):
+            a = np.zeros(o.n, np.uint32); a[i] = v; cases.append(a)
+    for abar in cases:
+        out = o.blind_rotate(K["brk"], acc, abar)
+        e = -sum(int(x) * int(y) for x, y in zip(abar, K["s"]))      # X^{-<a,s>}
+        assert np.array_equal(o.rlwe_phase(K["S"], out), o.monomial_mul(m, e))
+
+
+def test_blind_rotate_ternary_u(toy_cfg):
+    cfg = dict(toy_cfg, lwe_key="ternary")
+    o = Oracle(cfg, noiseless=True)
+    K = o.keys(23)
+    assert set(np.unique(K["s"])) <= {-1, 0, 1} and (K["s"] == -1).any()
+    m = np.random.default_rng(9).integers(0, o.Q, o.N, dtype=np.uint64)
+    acc = np.zeros((2, o.N), np.uint64); acc[0] = m
+    for abar in np.random.default_rng(10).integers(0, 2 * o.N, (20, o.n)).astype(np.uint32):
+        out = o.blind_rotate(K["brk"], acc, abar)
+        e = -sum(int(x) * int(y) for x, y in zip(abar, K["s"]))
+        assert np.array_equal(o.rlwe_phase(K["S"], out), o.monomial_mul(m, e))
+
+
+# ----------------------------------------------------------------------------- key switching
+def test_keyswitch_lwe_preserves_phase(toy_noiseless):
+    o, K = toy_noiseless
+    rng = np.random.default_rng(11)
+    sF = K["S"]
+    for _ in range(50):
+        a = rng.integers(0, o.q_lwe, o.N, dtype=np.uint64)
+        mu = int(rng.integers(0, o.q_lwe))
+        b = (sum(int(x) * int(y) for x, y in zip(a, sF)) + mu) % o.q_lwe
+        c = np.concatenate([[b], a]).astype(np.uint64)
+        out = o.keyswitch_lwe(K["ksk"], c)
+        assert o.lwe_phase(K["s"], out) == mu                   # PAPER.md:2039 (noiseless)
+
+
+def test_keyswitch_rlwe_preserves_phase(toy_noiseless):
+    o, K = toy_noiseless
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        a = rng.integers(0, o.Q, o.N, dtype=np.uint64)
+        mu = int(rng.integers(0, o.Q))
+        b = (sum(int(x) * int(y) for x, y in zip(a, K["S"])) + mu) % o.Q
+        c = np.concatenate([[b], a]).astype(np.uint64)
+        out = o.keyswitch_rlwe(K["bpk"], c)
+        ph = o.rlwe_phase(K["S"], out)
+        assert int(ph[0]) == mu and not ph[1:].any()
+
+
+def test_pubmux_selects(toy_noiseless):
+    o, K = toy_noiseless
+    rng = np.random.default_rng(13)
+    p0 = rng.integers(0, o.Q, o.N, dtype=np.uint64)
+    p1 = rng.integers(0, o.Q, o.N, dtype=np.uint64)
+    for bit in (0, 1):
+        accR = np.stack([o.rlwe_encrypt(40 + i, K["S"], np.eye(1, o.N, 0, dtype=np.uint64)[0] *
+                                        np.uint64((bit * o.L["boot"] ** i) % o.Q))[0]
+                         for i in range(o.ell["boot"])])
+        out = o.pubmux(accR, p0, p1)
+        assert np.array_equal(o.rlwe_phase(K["S"], out), p1 if bit else p0)
+
+
+# ----------------------------------------------------------------------------- SetupPolynomial (F6)
+@pytest.mark.parametrize("name", ["toy", "tiny", "fhew", "large"])
+def test_setup_polynomial_closed_form_and_theorem(name, toy_cfg):
+    cfg = toy_cfg if name == "toy" else synth.load_config(name)
+    o = Oracle(cfg)
+    N, Q, t = o.N, o.Q, o.t
+    bm = o.bootsmap(synth.lut(cfg))
+    p0, p1 = o.setup_polynomial(bm)
+    # closed form: every y in [0, 2N) written exactly once
+    e0, e1 = np.zeros(N, np.uint64), np.zeros(N, np.uint64)
+    for y in range(2 * N):
+        m = ((t * y + N) // (2 * N)) % t
+        v = int(bm[m])
+        if y == 0:
+            e0[0] = v
+        elif y < N:
+            e0[N - y] = (Q - v) % Q
+        elif y == N:
+            e1[0] = (Q - v) % Q
+        else:
+            e1[2 * N - y] = v
+    assert np.array_equal(p0, e0) and np.array_equal(p1, e1)
+    # Theorem: Coefs(rotP_x X^y)[1] = f(m) on each window
+    step, w = 2 * N // t, -(-N // t)
+    ys = range(2 * N) if N <= 256 else range(0, 2 * N, 37)
+    for y in ys:
+        m = ((y + w) // step) % t                                  # window of m: [step m - w, step m + w)
+        rot = o.monomial_mul(p0 if y < N else p1, y)
+        assert int(rot[0]) == int(bm[m])
+
+
+# ----------------------------------------------------------------------------- FDFB bootstrap
+@pytest.mark.parametrize("name", ["toy", "tiny"])
+def test_bootstrap_full_domain_noiseless(name, toy_cfg):
+    """Thm 2360-2394 with sigma = 0 and mod-switch-exact inputs: every m in Z_t maps to f(m)."""
+    cfg = toy_cfg if name == "toy" else synth.load_config(name)
+    o = Oracle(cfg, noiseless=True)
+    K = o.keys(cfg["seeds"]["keys"])
+    msgs = np.arange(o.t, dtype=np.uint64)
+    for lut_seed in (1, 2, 3):
+        f = synth.lut(cfg, seed=lut_seed)
+        rotp = o.setup_polynomial(o.bootsmap(f))
+        out = o.bootstrap(K, rotp, o.lwe_encrypt(7, K["s"], msgs, exact=True))
+        dec = [o.decode(o.lwe_phase(K["s"], c), o.q_lwe, o.t) for c in out]
+        assert dec == [int(f[m]) for m in msgs]
+
+
+def test_bootstrap_figure_wiring_fails(toy_cfg):
+    """F4: PubMux(rotP'_0, rotP'_1) in the figure's order selects the wrong half."""
+    o = Oracle(toy_cfg, noiseless=True)
+    K = o.keys(5)
+    f = synth.lut(toy_cfg, seed=4)
+    bm = o.bootsmap(f)
+    r0, r1 = o.setup_polynomial(bm)
+    N, Q, n = o.N, o.Q, o.n
+    wrong = 0
+    for m in range(o.t):
+        ct = o.lwe_encrypt(9, K["s"], [m], exact=True)[0]
+        bb = o.mod_switch(ct[0], o.q_lwe, 2 * N)
+        ab = np.array([o.mod_switch(x, o.q_lwe, 2 * N) for x in ct[1:]], np.uint32)
+        sgn = np.array([1] + [Q - 1] * (N - 1), np.uint64)
+        sgn = o.monomial_mul(sgn, bb)
+        h = (Q + 1) // 2
+        accR = []
+        for i in range(o.ell["boot"]):
+            c = pow(o.L["boot"], i, Q) * h % Q
+            acc = np.zeros((2, N), np.uint64); acc[0] = sgn * np.uint64(c) % np.uint64(Q)
+            acc[0] = np.array([int(x) * c % Q for x in sgn], np.uint64)
+            lwe = o.sample_extract(o.blind_rotate(K["brk"], acc, ab), 1)
+            lwe[0] = (int(lwe[0]) + c) % Q
+            accR.append(o.keyswitch_rlwe(K["bpk"], lwe))
+        accF = o.pubmux(np.stack(accR), o.monomial_mul(r0, bb), o.monomial_mul(r1, bb))  # figure order
+        cQ = o.sample_extract(o.blind_rotate(K["brk"], accF, ab), 1)
+        cq = np.array([o.mod_switch(x, Q, o.q_lwe) for x in cQ], np.uint64)
+        dec = o.decode(o.lwe_phase(K["s"], o.keyswitch_lwe(K["ksk"], cq)), o.q_lwe, o.t)
+        wrong += dec != int(f[m])
+    assert wrong > 0
+
+
+# ----------------------------------------------------------------------------- Pack / VectorPack / Shift
+@pytest.fixture
+def toy_pack(toy_cfg):
+    o = Oracle(toy_cfg, noiseless=True)
+    s, S = o.keygen_secrets(41)
+    pk = o.pack_key(42, S)
+    return o, S, pk
+
+
+def test_pack_and_vector_pack_message_law(toy_pack):
+    o, S, pk = toy_pack
+    rng = np.random.default_rng(14)
+    msg = rng.integers(0, o.Q, o.N, dtype=np.uint64)
+    ct = o.rlwe_encrypt(43, S, msg)[0]
+    v = np.stack([o.sample_extract(ct, k) for k in range(1, o.N + 1)])   # LWE of m_k under s_F
+    for d in (1, 5, o.N):
+        out = o.pack(pk, v[3], d)                             # m_4 lands at X^{d-1} (G5)
+        exp = np.zeros(o.N, np.uint64); exp[d - 1] = msg[3]
+        assert np.array_equal(o.rlwe_phase(S, out), exp)
+    for m in (1, 7, o.N):
+        out = o.vector_pack(pk, v[:m])
+        exp = np.zeros(o.N, np.uint64); exp[:m] = msg[:m]
+        assert np.array_equal(o.rlwe_phase(S, out), exp)
+
+
+def test_shift_is_cyclic_rotation_all_d(toy_pack):
+    """Lemma: m_out = cyclic rotation by d, for every d in [1, N-1]."""
+    o, S, pk = toy_pack
+    msg = np.random.default_rng(15).integers(0, o.Q, o.N, dtype=np.uint64)
+    ct = o.rlwe_encrypt(44, S, msg)[0]
+    for d in range(1, o.N):
+        exp = np.roll(msg, d)                                  # out[j] = m[(j - d) mod N]
+        assert np.array_equal(o.rlwe_phase(S, o.shift(pk, ct, d)), exp)
+    d = o.N // 2                                               # F3: both branches decrypt equally
+    a, b = o.shift(pk, ct, d), o.shift(pk, ct, d, force_branch2=True)
+    assert not np.array_equal(a, b)
+    assert np.array_equal(o.rlwe_phase(S, a), o.rlwe_phase(S, b))
+
+
+def test_shift_l2_error_bound_noisy(toy_cfg):
+    """G15 / F9: ||e_out||_2 <= ||e_ct||_2 + N^2 ell max||e_pK||_2, checked per instance."""
+    o = Oracle(toy_cfg)
+    s, S = o.keygen_secrets(51)
+    pk = o.pack_key(52, S)
+    N, Q = o.N, o.Q
+    emax = 0.0
+    for i in range(N):
+        for j in range(o.ell["pack"]):
+            for k in range(o.L_pack):
+                ph = o.rlwe_phase(S, pk[i, j, k])
+                ph[0] = (int(ph[0]) - int(S[i]) * (1 << j) * k) % Q
+                emax = max(emax, math.sqrt(sum(centered(x, Q) ** 2 for x in ph)))
+    msg = np.random.default_rng(16).integers(0, Q, N, dtype=np.uint64)
+    ct = o.rlwe_encrypt(53, S, msg)[0]
+    ect = math.sqrt(sum(centered(int(p) - int(m), Q) ** 2 for p, m in zip(o.rlwe_phase(S, ct), msg)))
+    for d in range(1, N):
+        out = o.shift(pk, ct, d)
+        e = [centered(int(p) - int(m), Q) for p, m in zip(o.rlwe_phase(S, out), np.roll(msg, d))]
+        assert math.sqrt(sum(x * x for x in e)) <= ect + N * N * o.ell["pack"] * emax
