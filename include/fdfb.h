@@ -1,0 +1,174 @@
+/*
+ * fdfb.h -- C-ABI of the B200 (sm_100a) FDFB hot-path library libfdfb.so.
+ *
+ * Paper: "FDFB: Full Domain Functional Bootstrapping Towards Practical Fully
+ * Homomorphic Encryption" (arXiv 2109.02731); line numbers are PAPER.md lines.
+ *
+ * Conventions (all entry points):
+ *   - Every compute call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*, NULL = legacy default stream) and never synchronises the host,
+ *     except fdfb_ctx_create / fdfb_keygen* / fdfb_*_host which say so.
+ *   - Buffers marked [dev] are caller-owned device memory, [host] host memory.
+ *     The library keeps no pointer to caller memory after a call returns.
+ *   - Return value: FDFB_OK (0) or a negative FDFB_E_* status; arguments are
+ *     validated before any launch, so an error return means nothing ran,
+ *     except FDFB_E_CUDA (a launch or runtime call failed; see
+ *     fdfb_last_cuda_error).  Nothing throws across the ABI.
+ *   - Ciphertext layouts (canonical, coefficient domain, residues canonical):
+ *       LWE  [b, a_1..a_n] as uint64, mod q_lwe = 2^log_q_lwe (inputs/outputs
+ *            of bootstrap/keyswitch) or mod Q (SampleExt outputs, VectorPack
+ *            inputs)
+ *       RLWE [b_0..b_{N-1}, a_0..a_{N-1}] uint64 mod Q
+ *   - Key layouts on the device are OPAQUE (NTT domain, Shoup companions,
+ *     suffix sums); fdfb_key_import/fdfb_keygen_canonical translate from/to the
+ *     canonical layouts documented in DESIGN.md ("Canonical layouts").
+ *   - Indices k (SampleExt) and d (Shift) are 1-based, as in the paper.
+ */
+#ifndef FDFB_H
+#define FDFB_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+enum {
+  FDFB_OK = 0,
+  FDFB_E_NULL = -1,                 /* a required pointer is NULL                        */
+  FDFB_E_NON_NTT_MODULUS = -2,      /* Q not prime or Q != 1 mod 2N          */
+  FDFB_E_DIMENSION = -3,            /* N not in {256,512,1024,2048}, n out of range       */
+  FDFB_E_DECOMP = -4,               /* ell != ceil(bits/logL) for some gadget             */
+  FDFB_E_INDEX = -5,                /* SampleExt k or Shift d out of range                */
+  FDFB_E_PLAINTEXT = -6,            /* t does not divide 2N, t_out == 0                   */
+  FDFB_E_UNSUPPORTED = -7,          /* combination not implemented                        */
+  FDFB_E_CUDA = -8,                 /* CUDA runtime / launch failure                      */
+  FDFB_E_WORKSPACE = -9,            /* workspace too small                                */
+  FDFB_E_KIND = -10                 /* unknown key kind                                   */
+};
+
+/* ------------------------------------------------------------------ params */
+typedef struct fdfb_params {
+  uint32_t N;          /* ring degree, power of two in [256, 2048]                         */
+  uint32_t n;          /* LWE dimension, 1..4096                                           */
+  uint64_t Q;          /* RLWE prime, Q = 1 mod 2N, Q < 2^62              */
+  uint32_t log_q_lwe;  /* LWE modulus q_lwe = 2^log_q_lwe, 8..62 (reading c.3)   */
+  uint32_t lwe_key;    /* 0: binary s, u = [1];  1: ternary s, u = [-1, 1] */
+  uint32_t rlwe_key;   /* 0: binary, 1: ternary ring secret                                */
+  uint32_t logL_rgsw, ell_rgsw;   /* brK gadget   (L = 2^logL, ell = ceil(log_L Q))       */
+  uint32_t logL_boot, ell_boot;   /* sign ladder / PubMux base L_boot     */
+  uint32_t logL_pk, ell_pk;       /* bootstrap LWE->RLWE key pK            */
+  uint32_t logL_ks, ell_ks;       /* LWE->LWE key ksK mod q_lwe            */
+  uint32_t logL_pack, ell_pack;   /* Shift packing key               */
+  uint32_t t;          /* plaintext modulus of bootstrap inputs, t | 2N                    */
+  uint32_t sigma_milli;/* Gaussian sigma * 1000 (3200), 0 = noiseless keys (tests)         */
+} fdfb_params;
+
+typedef struct fdfb_ctx fdfb_ctx;
+
+/* Key kinds for fdfb_key_import / fdfb_keygen_canonical. Canonical layouts:
+ *   BRK  [n][u][2*ell_rgsw][2][N]   RGSW rows, row r<ell: b-gadget
+ *   BPK  [N][ell_pk][2][N]          RLWE_s(s_F[i] L^j)
+ *   KSK  [N][ell_ks][n+1]           LWE_s(s_F[i] L^j) mod q_lwe
+ *   PACK [N][ell_pack][L_pack][2][N] RLWE_s(s_F[i] L^j k)
+ *   SK_LWE int8[n], SK_RLWE int8[N]                                             */
+enum { FDFB_KEY_BRK = 1, FDFB_KEY_BPK = 2, FDFB_KEY_KSK = 3, FDFB_KEY_PACK = 4,
+       FDFB_KEY_SK_LWE = 5, FDFB_KEY_SK_RLWE = 6 };
+
+typedef struct fdfb_sizes_t {
+  size_t sk_lwe, sk_rlwe;       /* bytes of the int8 secrets                        */
+  size_t brk, bpk, ksk, pack;   /* bytes of the OPAQUE device key formats            */
+  size_t canon_brk, canon_bpk, canon_ksk, canon_pack;  /* canonical layouts (bytes) */
+} fdfb_sizes_t;
+
+/* Create a context on `device`: validates params (FDFB_E_*), derives 2N-th roots,
+ * twiddle tables and the CDT table, uploads them.  Synchronises the device. */
+int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out);
+void fdfb_ctx_destroy(fdfb_ctx* ctx);
+int fdfb_sizes(const fdfb_ctx* ctx, fdfb_sizes_t* out);
+/* Workspace bytes needed by fdfb_bootstrap_batch / fdfb_shift / fdfb_vector_pack for B items. */
+size_t fdfb_workspace_bootstrap(const fdfb_ctx* ctx, uint32_t B);
+size_t fdfb_workspace_shift(const fdfb_ctx* ctx, uint32_t B);
+size_t fdfb_workspace_vector_pack(const fdfb_ctx* ctx, uint32_t m, uint32_t B);
+
+/* ------------------------------------------------------------------ keys
+ * Keygen from a 64-bit seed with the counter-based Philox4x64-10 sampling spec of
+ * DESIGN.md ("Seeded determinism"): BRKeyGen, KeySwitchSetup
+ * for pK and ksK (2369-2371, 2992-3001), PackSetup (1284-1296).  which: bitmask
+ * 1=secrets 2=brk 4=bpk 8=ksk 16=pack; pointers of unselected keys may be NULL,
+ * but brk/bpk/ksk/pack need the secrets in sk_lwe/sk_rlwe [dev] (generated in the
+ * same call if bit 1 is set).  Allocates and frees device temporaries; syncs. */
+int fdfb_keygen(const fdfb_ctx* ctx, uint64_t seed, uint32_t which, int8_t* sk_lwe, int8_t* sk_rlwe,
+                void* brk, void* bpk, void* ksk, void* pack, void* stream);
+/* Canonical key entries for parity checks: `count` entries with flat canonical entry
+ * indices idx[] [host] (BRK: (i*u+j)*2ell+row; BPK/KSK: i*ell+j; PACK: (i*ell+j)*L+k),
+ * written back to back into out [dev] (2N words per RLWE entry, n+1 per LWE entry). */
+int fdfb_keygen_canonical(const fdfb_ctx* ctx, uint64_t seed, int kind, const int8_t* sk_lwe,
+                          const int8_t* sk_rlwe, const uint64_t* idx, uint32_t count, uint64_t* out,
+                          void* stream);
+/* Convert a canonical key [dev] to the opaque device format [dev].  Syncs. */
+int fdfb_key_import(const fdfb_ctx* ctx, int kind, const uint64_t* canonical, void* dev_key, void* stream);
+
+/* ------------------------------------------------------------------ inputs
+ * LWE encryptions of m[c] in Z_t (Delta = q_lwe/t) under sk_lwe,
+ * object c of domain 7.  flags bit0: mod-switch-exact inputs. */
+int fdfb_lwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_lwe, const uint64_t* msg,
+                     uint32_t count, uint32_t flags, uint64_t* out, void* stream);
+/* RLWE encryptions of message polynomials msg [dev, count x N] (domain 8). */
+int fdfb_rlwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_rlwe, const uint64_t* msg,
+                      uint32_t count, uint64_t* out, void* stream);
+
+/* ------------------------------------------------------------------ LUT
+ * BootsMap[x] = round(Q/t_out) * lut[x] then SetupPolynomial
+ * (Fig. SetupPolynomial, half-open windows, reading F6).
+ * lut [host, t values in Z_t_out]; rotp [dev, 2 x N] = (rotP_0, rotP_1). */
+int fdfb_setup_lut(const fdfb_ctx* ctx, const uint64_t* lut, uint32_t t_out, uint64_t* rotp, void* stream);
+
+/* ------------------------------------------------------------------ hot path
+ * FDFB Bootstrap (Fig. Bootstrap; readings R1, F4, c.3):
+ * ct_in [dev, B x (n+1)] mod q_lwe -> ct_out [dev, B x (n+1)] mod q_lwe encrypting
+ * f(m).  workspace [dev] of fdfb_workspace_bootstrap(ctx, B) bytes. */
+int fdfb_bootstrap_batch(const fdfb_ctx* ctx, const void* brk, const void* bpk, const void* ksk,
+                         const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
+                         void* workspace, void* stream);
+/* Same, with ct_in/ct_out in (pinned) HOST memory: H2D copy, bootstrap, D2H copy,
+ * all on `stream`; synchronises the stream before returning. */
+int fdfb_bootstrap_batch_host(const fdfb_ctx* ctx, const void* brk, const void* bpk, const void* ksk,
+                              const uint64_t* rotp, const uint64_t* ct_in_host, uint64_t* ct_out_host,
+                              uint32_t B, void* workspace, void* stream);
+/* BlindRotate: acc [dev, count x 2 x N] in/out, abar [dev,
+ * count x n] in Z_2N; accumulator g uses abar row g / acc_per_ct. */
+int fdfb_blind_rotate(const fdfb_ctx* ctx, const void* brk, uint64_t* acc, const uint32_t* abar,
+                      uint32_t count, uint32_t acc_per_ct, void* stream);
+/* SampleExt (NSgn(0) = -1): rlwe [dev, B x 2N], k [dev, B, 1..N],
+ * lwe [dev, B x (N+1)] mod Q. */
+int fdfb_sample_extract(const fdfb_ctx* ctx, const uint64_t* rlwe, const uint32_t* k, uint64_t* lwe,
+                        uint32_t B, void* stream);
+/* LWE KeySwitch N -> n mod q_lwe: in [dev, B x (N+1)] mod q_lwe. */
+int fdfb_lwe_keyswitch(const fdfb_ctx* ctx, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
+                       uint32_t B, void* stream);
+/* VectorPack: lwe [dev, B x m x (N+1)] mod Q under s_F,
+ * 1 <= m <= N; out [dev, B x 2N]. */
+int fdfb_vector_pack(const fdfb_ctx* ctx, const void* pack, const uint64_t* lwe, uint32_t m, uint64_t* out,
+                     uint32_t B, void* workspace, void* stream);
+/* Shift (readings F2/F3): rlwe_in [dev, B x 2N], d [dev, B, 1..N-1]. */
+int fdfb_shift(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* d,
+               uint64_t* rlwe_out, uint32_t B, void* workspace, void* stream);
+
+/* ------------------------------------------------------------------ kernel unit tests
+ * Negacyclic ring product through the NTT kernels: c = a * b mod (X^N+1, Q),
+ * a, b, c [dev, count x N]. */
+int fdfb_poly_mul(const fdfb_ctx* ctx, const uint64_t* a, const uint64_t* b, uint64_t* c, uint32_t count,
+                  void* stream);
+/* The library's own CDT thresholds (2T values) into thr [host]; *T = tail cut. */
+int fdfb_cdt_table(const fdfb_ctx* ctx, uint64_t* thr, int* T);
+/* Number of kernel launches issued by this context so far (bench evidence). */
+uint64_t fdfb_launch_count(const fdfb_ctx* ctx);
+const char* fdfb_status_string(int status);
+const char* fdfb_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDFB_H */

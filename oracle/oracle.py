@@ -24,7 +24,7 @@ P_FIELDS = ["N", "n", "Q", "log_q_lwe", "lwe_key", "rlwe_key", "logL_rgsw", "ell
 
 def build_oracle(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-march=native", "-fopenmp", "-fPIC", "-shared",
+        subprocess.check_call(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared",
                                "-o", _LIB, _SRC])
     return _LIB
 

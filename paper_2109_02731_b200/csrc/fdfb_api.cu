@@ -1,0 +1,679 @@
+// fdfb_api.cu -- the C-ABI of libfdfb.so (include/fdfb.h): parameter validation,
+// context setup (roots of unity, twiddles, CDT), key generation/import and the
+// stream-ordered orchestration of the hot-path kernels.  Unity build: the kernel
+// headers are included here.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fdfb.h"
+#include "kernels_boot.cuh"
+#include "kernels_shift.cuh"
+
+typedef unsigned __int128 u128;
+
+struct fdfb_ctx {
+  fdfb_params prm;
+  DevParams dp;
+  int device;
+  int num_sms;
+  u64 qinv_neg, r2;          // Montgomery constants
+  u64* d_tables;             // tw | twp | itw | itwp | cdt | omega tables
+  u64 omega_off;             // offset of NTT(X) slots (omega) in d_tables
+  std::vector<u64> cdt;
+  mutable std::atomic<unsigned long long> launches{0};
+};
+
+static thread_local std::string g_last_cuda;
+
+#define CK(x)                                                              \
+  do {                                                                     \
+    cudaError_t _e = (x);                                                  \
+    if (_e != cudaSuccess) {                                               \
+      g_last_cuda = std::string(#x) + ": " + cudaGetErrorString(_e);       \
+      return FDFB_E_CUDA;                                                  \
+    }                                                                      \
+  } while (0)
+#define CKL(ctx)                                                           \
+  do {                                                                     \
+    (ctx)->launches++;                                                     \
+    cudaError_t _e = cudaGetLastError();                                   \
+    if (_e != cudaSuccess) {                                               \
+      g_last_cuda = std::string("launch: ") + cudaGetErrorString(_e);      \
+      return FDFB_E_CUDA;                                                  \
+    }                                                                      \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+// ------------------------------------------------------------------ host number theory
+static u64 h_mulmod(u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); }
+static u64 h_powmod(u64 b, u64 e, u64 m) {
+  u64 r = 1 % m; b %= m;
+  while (e) { if (e & 1) r = h_mulmod(r, b, m); b = h_mulmod(b, b, m); e >>= 1; }
+  return r;
+}
+static bool h_is_prime(u64 n) {   // deterministic Miller-Rabin for 64-bit
+  if (n < 2) return false;
+  for (u64 p : {2ULL, 3ULL, 5ULL, 7ULL, 11ULL, 13ULL, 17ULL, 19ULL, 23ULL, 29ULL, 31ULL, 37ULL}) {
+    if (n % p == 0) return n == p;
+  }
+  u64 d = n - 1; int s = 0;
+  while ((d & 1) == 0) { d >>= 1; s++; }
+  for (u64 a : {2ULL, 3ULL, 5ULL, 7ULL, 11ULL, 13ULL, 17ULL, 19ULL, 23ULL, 29ULL, 31ULL, 37ULL}) {
+    u64 x = h_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int r = 1; r < s; r++) { x = h_mulmod(x, x, n); if (x == n - 1) { comp = false; break; } }
+    if (comp) return false;
+  }
+  return true;
+}
+static int bits_of(u64 x) { int b = 0; while (b < 64 && (x >> b)) b++; return b; }   // ceil(log2(x+1))
+static int ceil_log2(u64 x) { int b = 0; while ((1ULL << b) < x) b++; return b; }
+static u64 shoup_of(u64 w, u64 Q) { return (u64)(((u128)w << 64) / Q); }
+static int bitrev(int x, int logn) { int r = 0; for (int i = 0; i < logn; i++) r |= ((x >> i) & 1) << (logn - 1 - i); return r; }
+
+// Library-side CDT for sigma = sigma_milli/1000, support [-T, T], T = floor(6 sigma):
+// thr[k] = floor(2^64 CDF(-T + k)), computed in long double.
+static std::vector<u64> make_cdt(uint32_t sigma_milli, int* Tout) {
+  std::vector<u64> thr;
+  if (sigma_milli == 0) { *Tout = 0; return thr; }
+  long double sg = sigma_milli / 1000.0L;
+  int T = (int)floorl(6 * sg);
+  std::vector<long double> rho;
+  long double Z = 0;
+  for (int e = -T; e <= T; e++) { long double r = expl(-(long double)e * e / (2 * sg * sg)); rho.push_back(r); Z += r; }
+  long double acc = 0;
+  for (int k = 0; k < 2 * T; k++) {
+    acc += rho[k];
+    long double v = ldexpl(acc / Z, 64);
+    thr.push_back(v >= ldexpl(1.0L, 64) ? ~0ULL : (u64)floorl(v));
+  }
+  *Tout = T;
+  return thr;
+}
+
+// ------------------------------------------------------------------ launch helpers
+static int grid_for(size_t total, int threads, int num_sms) {
+  size_t g = (total + threads - 1) / threads;
+  size_t cap = (size_t)num_sms * 32;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <int N>
+static int launch_ntt_batch_t(const fdfb_ctx* c, u64* data, int count, int mode, cudaStream_t st) {
+  constexpr int T = N / 8;
+  int G = T >= 256 ? 1 : 256 / T;
+  dim3 blk(T, G);
+  dim3 grd((count + G - 1) / G);
+  size_t sm = (size_t)G * N * sizeof(u64);
+  k_ntt_batch<N><<<grd, blk, sm, st>>>(c->dp, data, count, mode);
+  CKL(c);
+  return FDFB_OK;
+}
+static int launch_ntt_batch(const fdfb_ctx* c, u64* data, size_t count, int mode, cudaStream_t st) {
+  // chunk to keep grid.x within limits
+  const size_t CH = 1 << 20;
+  for (size_t o = 0; o < count; o += CH) {
+    int cnt = (int)((count - o) < CH ? (count - o) : CH);
+    u64* d = data + o * c->prm.N;
+    int rc;
+    switch (c->prm.N) {
+      case 256: rc = launch_ntt_batch_t<256>(c, d, cnt, mode, st); break;
+      case 512: rc = launch_ntt_batch_t<512>(c, d, cnt, mode, st); break;
+      case 1024: rc = launch_ntt_batch_t<1024>(c, d, cnt, mode, st); break;
+      case 2048: rc = launch_ntt_batch_t<2048>(c, d, cnt, mode, st); break;
+      default: return FDFB_E_DIMENSION;
+    }
+    if (rc) return rc;
+  }
+  return FDFB_OK;
+}
+
+template <int N>
+static int launch_br_t(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
+                       cudaStream_t st) {
+  constexpr int T = N / 8;
+  size_t sm = 4 * N * sizeof(u64);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_blind_rotate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr_set = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate<N>, T, sm);
+  if (per_sm < 1) per_sm = 1;
+  int grid = c->num_sms * per_sm;
+  if (grid > n_acc) grid = n_acc;
+  k_blind_rotate<N><<<grid, T, sm, st>>>(c->dp, bsk, accs, n_acc, acc_per_ct, abar);
+  CKL(c);
+  return FDFB_OK;
+}
+static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
+                     cudaStream_t st) {
+  if (n_acc <= 0) return FDFB_OK;
+  switch (c->prm.N) {
+    case 256: return launch_br_t<256>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
+    case 512: return launch_br_t<512>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
+    case 1024: return launch_br_t<1024>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
+    case 2048: return launch_br_t<2048>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
+  }
+  return FDFB_E_DIMENSION;
+}
+
+// ------------------------------------------------------------------ context
+static int validate(const fdfb_params* p) {
+  if (!p) return FDFB_E_NULL;
+  if (!(p->N == 256 || p->N == 512 || p->N == 1024 || p->N == 2048)) return FDFB_E_DIMENSION;
+  if (p->n < 1 || p->n > 4096) return FDFB_E_DIMENSION;
+  if (p->Q < 3 || p->Q >= (1ULL << 56) || !h_is_prime(p->Q) || (p->Q - 1) % (2 * (u64)p->N)) return FDFB_E_NON_NTT_MODULUS;
+  if (p->log_q_lwe < 8 || p->log_q_lwe > 62 || p->log_q_lwe < (uint32_t)ceil_log2(2 * p->N) + 1) return FDFB_E_DIMENSION;
+  if (p->lwe_key > 1 || p->rlwe_key > 1) return FDFB_E_UNSUPPORTED;
+  const int qb = bits_of(p->Q - 1) > 0 ? ceil_log2(p->Q) : 1;
+  auto ok = [](uint32_t logL, uint32_t ell, int bits) {
+    return logL >= 1 && logL <= 32 && ell >= 1 && (int)ell == (bits + (int)logL - 1) / (int)logL;
+  };
+  if (!ok(p->logL_rgsw, p->ell_rgsw, qb) || p->ell_rgsw > 8) return FDFB_E_DECOMP;
+  if (!ok(p->logL_boot, p->ell_boot, qb) || p->ell_boot > 64) return FDFB_E_DECOMP;
+  if (!ok(p->logL_pk, p->ell_pk, qb)) return FDFB_E_DECOMP;
+  if (!ok(p->logL_ks, p->ell_ks, (int)p->log_q_lwe)) return FDFB_E_DECOMP;
+  if (!ok(p->logL_pack, p->ell_pack, qb) || p->logL_pack > 12) return FDFB_E_DECOMP;
+  if ((u128)p->N * p->ell_pk * (1ULL << p->logL_pk) >= ((u128)1 << 32)) return FDFB_E_DECOMP;
+  if (p->t < 2 || (2 * p->N) % p->t) return FDFB_E_PLAINTEXT;
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out) {
+  if (!out) return FDFB_E_NULL;
+  *out = nullptr;
+  int rc = validate(p);
+  if (rc) return rc;
+  CK(cudaSetDevice(device));
+  fdfb_ctx* c = new fdfb_ctx();
+  c->prm = *p;
+  c->device = device;
+  CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  const u64 Q = p->Q;
+  const int N = p->N, logN = ceil_log2(N);
+  // primitive 2N-th root of unity: psi = g^{(Q-1)/2N} with psi^N = -1
+  u64 psi = 0;
+  for (u64 g = 2; g < 1000; g++) {
+    u64 c2 = h_powmod(g, (Q - 1) / (2 * (u64)N), Q);
+    if (h_powmod(c2, N, Q) == Q - 1) { psi = c2; break; }
+  }
+  if (!psi) { delete c; return FDFB_E_NON_NTT_MODULUS; }
+  u64 psi_inv = h_powmod(psi, Q - 2, Q);
+  int T = 0;
+  c->cdt = make_cdt(p->sigma_milli, &T);
+  // tables: tw, twp, itw, itwp (N each), cdt (2T), omega (N)
+  size_t ntab = 4 * (size_t)N + c->cdt.size() + N;
+  std::vector<u64> h(ntab, 0);
+  for (int k = 0; k < N; k++) {
+    int br = bitrev(k, logN);
+    u64 w = h_powmod(psi, br, Q), wi = h_powmod(psi_inv, br, Q);
+    h[k] = w; h[N + k] = shoup_of(w, Q);
+    h[2 * N + k] = wi; h[3 * N + k] = shoup_of(wi, Q);
+  }
+  for (size_t k = 0; k < c->cdt.size(); k++) h[4 * N + k] = c->cdt[k];
+  // omega[slot] = value of X at the slot's evaluation point = psi^{2 bitrev(slot) + 1}
+  c->omega_off = 4 * (size_t)N + c->cdt.size();
+  for (int k = 0; k < N; k++) h[c->omega_off + k] = h_powmod(psi, 2 * (u64)bitrev(k, logN) + 1, Q);
+  CK(cudaMalloc(&c->d_tables, ntab * sizeof(u64)));
+  CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
+  DevParams& d = c->dp;
+  memset(&d, 0, sizeof(d));
+  d.Q = Q; d.Q2 = 2 * Q; d.Q4 = 4 * Q; d.half = (Q + 1) / 2;
+  d.q_mask = (p->log_q_lwe >= 64) ? ~0ULL : ((1ULL << p->log_q_lwe) - 1);
+  d.N = N; d.logN = logN; d.n = p->n; d.u = p->lwe_key ? 2 : 1;
+  d.log_q_lwe = p->log_q_lwe;
+  d.logL_rgsw = p->logL_rgsw; d.ell_rgsw = p->ell_rgsw;
+  d.logL_boot = p->logL_boot; d.ell_boot = p->ell_boot;
+  d.logL_pk = p->logL_pk; d.ell_pk = p->ell_pk;
+  d.logL_ks = p->logL_ks; d.ell_ks = p->ell_ks;
+  d.logL_pack = p->logL_pack; d.ell_pack = p->ell_pack;
+  d.lwe_ternary = p->lwe_key; d.rlwe_ternary = p->rlwe_key;
+  d.noiseless = p->sigma_milli == 0; d.cdt_T = T;
+  d.t = p->t;
+  d.tw = c->d_tables; d.twp = c->d_tables + N; d.itw = c->d_tables + 2 * N; d.itwp = c->d_tables + 3 * N;
+  d.cdt = c->d_tables + 4 * N;
+  d.ninv = h_powmod(N, Q - 2, Q); d.ninvp = shoup_of(d.ninv, Q);
+  // Montgomery: -Q^{-1} mod 2^64 (Newton), R^2 mod Q
+  u64 inv = 1;
+  for (int i = 0; i < 7; i++) inv *= 2 - Q * inv;
+  c->qinv_neg = 0 - inv;
+  u64 r1 = (u64)(((u128)1 << 64) % Q);
+  c->r2 = h_mulmod(r1, r1, Q);
+  *out = c;
+  return FDFB_OK;
+}
+
+extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
+  if (!c) return;
+  cudaFree(c->d_tables);
+  delete c;
+}
+
+static size_t brk_words(const fdfb_params& p) { return (size_t)p.n * (p.lwe_key ? 2 : 1) * 2 * p.ell_rgsw * 2 * p.N; }
+
+extern "C" int fdfb_sizes(const fdfb_ctx* c, fdfb_sizes_t* o) {
+  if (!c || !o) return FDFB_E_NULL;
+  const fdfb_params& p = c->prm;
+  o->sk_lwe = p.n; o->sk_rlwe = p.N;
+  o->canon_brk = brk_words(p) * 8;
+  o->brk = o->canon_brk * 2;
+  o->canon_bpk = (size_t)p.N * p.ell_pk * 2 * p.N * 8;
+  o->bpk = o->canon_bpk;
+  o->canon_ksk = (size_t)p.N * p.ell_ks * (p.n + 1) * 8;
+  o->ksk = o->canon_ksk;
+  o->canon_pack = (size_t)p.N * p.ell_pack * (1ULL << p.logL_pack) * 2 * p.N * 8;
+  o->pack = shift_pack_bytes(p);
+  return FDFB_OK;
+}
+
+// workspace layout of fdfb_bootstrap_batch
+struct BootWs {
+  u32* abar; u32* bbar; u64* accs; u64* lweN; u64* dig; u64* F; size_t bytes;
+};
+static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base) {
+  BootWs w;
+  char* b = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = b + off; off += (bytes + 255) & ~(size_t)255; return r; };
+  const size_t ellb = p.ell_boot, N = p.N;
+  w.abar = (u32*)take((size_t)B * p.n * 4);
+  w.bbar = (u32*)take((size_t)B * 4);
+  w.accs = (u64*)take((size_t)B * ellb * 2 * N * 8);
+  w.lweN = (u64*)take((size_t)B * ellb * (N + 1) * 8);
+  w.dig = (u64*)take((size_t)B * ellb * N * 8);
+  w.F = (u64*)take((size_t)B * 2 * N * 8);
+  w.bytes = off;
+  return w;
+}
+extern "C" size_t fdfb_workspace_bootstrap(const fdfb_ctx* c, uint32_t B) {
+  if (!c) return 0;
+  return boot_ws(c->prm, B, nullptr).bytes + (size_t)B * 2 * (c->prm.n + 1) * 8;  // + host staging
+}
+
+// ------------------------------------------------------------------ encryption helpers
+// Encrypt `count` canonical RLWE entries of `kind` (BRK/BPK/PACK) into out [count][2][N].
+static int rlwe_entries(const fdfb_ctx* c, u64 seed, int kind, const int8_t* s_lwe, const int8_t* s_rlwe,
+                        const u64* idx, u64 idx_base, int count, u64* out, u64* shat, u64* tmp_mask,
+                        u64* tmp_prod, cudaStream_t st) {
+  const int N = c->prm.N;
+  dim3 g1((N + 255) / 256, count);
+  k_rlwe_mask<<<g1, 256, 0, st>>>(c->dp, kind, idx, idx_base, count, seed, s_lwe, s_rlwe, tmp_mask);
+  CKL(c);
+  CK(cudaMemcpyAsync(tmp_prod, tmp_mask, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
+  int rc = launch_ntt_batch(c, tmp_prod, count, 0, st);
+  if (rc) return rc;
+  size_t tot = (size_t)count * N;
+  k_pointwise_mul<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(tmp_prod, shat, tmp_prod, tot, N, c->dp.Q,
+                                                                   c->qinv_neg, c->r2);
+  CKL(c);
+  rc = launch_ntt_batch(c, tmp_prod, count, 1, st);
+  if (rc) return rc;
+  k_rlwe_finish<<<g1, 256, 0, st>>>(c->dp, kind, idx, idx_base, count, seed, s_lwe, s_rlwe, tmp_mask, tmp_prod, out);
+  CKL(c);
+  return FDFB_OK;
+}
+
+__global__ void k_secret_to_residues(DevParams p, const int8_t* s, u64* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < p.N) out[i] = from_signed(s[i], p.Q);
+}
+static int make_shat(const fdfb_ctx* c, const int8_t* s_rlwe, u64* shat, cudaStream_t st) {
+  k_secret_to_residues<<<(c->prm.N + 255) / 256, 256, 0, st>>>(c->dp, s_rlwe, shat);
+  CKL(c);
+  return launch_ntt_batch(c, shat, 1, 0, st);
+}
+
+// canonical brk rows [rows][2][N] (coef) -> device BRK; rows are consecutive canonical rows
+// starting at row0 (flat (i*u+j)*2ell + row).  tmp: rows*2*N words.
+static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, size_t row0, u64* dev, u64* tmp,
+                           cudaStream_t st) {
+  const int N = c->prm.N;
+  CK(cudaMemcpyAsync(tmp, canon, rows * 2 * N * 8, cudaMemcpyDeviceToDevice, st));
+  int rc = launch_ntt_batch(c, tmp, rows * 2, 0, st);
+  if (rc) return rc;
+  size_t tot = rows * 2 * N;
+  k_brk_finalize<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, tmp, dev + row0 * 2 * 2 * N, rows * 2);
+  CKL(c);
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int8_t* sk_lwe, int8_t* sk_rlwe,
+                           void* brk, void* bpk, void* ksk, void* pack, void* stream) {
+  if (!c) return FDFB_E_NULL;
+  cudaStream_t st = S(stream);
+  const fdfb_params& p = c->prm;
+  const int N = p.N;
+  if (!sk_lwe || !sk_rlwe) return FDFB_E_NULL;
+  if (((which & 2) && !brk) || ((which & 4) && !bpk) || ((which & 8) && !ksk) || ((which & 16) && !pack))
+    return FDFB_E_NULL;
+  if (which & 1) {
+    int m = p.n > p.N ? p.n : p.N;
+    k_keygen_secrets<<<(m + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe);
+    CKL(c);
+  }
+  const int CH = 2048;  // RLWE entries per chunk
+  u64 *shat = nullptr, *tmask = nullptr, *tprod = nullptr, *tout = nullptr, *tntt = nullptr;
+  CK(cudaMallocAsync(&shat, (size_t)N * 8, st));
+  CK(cudaMallocAsync(&tmask, (size_t)CH * N * 8, st));
+  CK(cudaMallocAsync(&tprod, (size_t)CH * N * 8, st));
+  CK(cudaMallocAsync(&tout, (size_t)CH * 2 * N * 8, st));
+  CK(cudaMallocAsync(&tntt, (size_t)CH * 2 * N * 8, st));
+  int rc = make_shat(c, sk_rlwe, shat, st);
+  if (!rc && (which & 2)) {
+    size_t rows = brk_words(p) / (2 * (size_t)N);
+    for (size_t o = 0; o < rows && !rc; o += CH) {
+      int cnt = (int)((rows - o) < (size_t)CH ? (rows - o) : CH);
+      rc = rlwe_entries(c, seed, 1, sk_lwe, sk_rlwe, nullptr, o, cnt, tout, shat, tmask, tprod, st);
+      if (!rc) rc = brk_import_rows(c, tout, cnt, o, (u64*)brk, tntt, st);
+    }
+  }
+  if (!rc && (which & 4)) {
+    size_t ent = (size_t)N * p.ell_pk;
+    for (size_t o = 0; o < ent && !rc; o += CH) {
+      int cnt = (int)((ent - o) < (size_t)CH ? (ent - o) : CH);
+      rc = rlwe_entries(c, seed, 2, sk_lwe, sk_rlwe, nullptr, o, cnt, (u64*)bpk + o * 2 * N, shat, tmask, tprod, st);
+    }
+  }
+  if (!rc && (which & 8)) {
+    int ent = N * p.ell_ks;
+    k_ksk_gen<<<(ent * 32 + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe, nullptr, 0, ent, (u64*)ksk);
+    CKL(c);
+  }
+  if (!rc && (which & 16)) rc = pack_keygen(c, seed, sk_rlwe, pack, shat, tmask, tprod, tout, CH, st);
+  cudaFreeAsync(shat, st); cudaFreeAsync(tmask, st); cudaFreeAsync(tprod, st); cudaFreeAsync(tout, st);
+  cudaFreeAsync(tntt, st);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(st));
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_keygen_canonical(const fdfb_ctx* c, uint64_t seed, int kind, const int8_t* sk_lwe,
+                                     const int8_t* sk_rlwe, const uint64_t* idx, uint32_t count, uint64_t* out,
+                                     void* stream) {
+  if (!c || !idx || !out || !sk_lwe || !sk_rlwe) return FDFB_E_NULL;
+  if (count == 0) return FDFB_OK;
+  cudaStream_t st = S(stream);
+  const int N = c->prm.N;
+  u64* didx = nullptr;
+  CK(cudaMallocAsync(&didx, (size_t)count * 8, st));
+  CK(cudaMemcpyAsync(didx, idx, (size_t)count * 8, cudaMemcpyHostToDevice, st));
+  int rc = FDFB_OK;
+  if (kind == FDFB_KEY_KSK) {
+    k_ksk_gen<<<(count * 32 + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe, didx, 0, count, out);
+    CKL(c);
+  } else if (kind == FDFB_KEY_BRK || kind == FDFB_KEY_BPK || kind == FDFB_KEY_PACK) {
+    u64 *shat, *tm, *tp;
+    CK(cudaMallocAsync(&shat, (size_t)N * 8, st));
+    CK(cudaMallocAsync(&tm, (size_t)count * N * 8, st));
+    CK(cudaMallocAsync(&tp, (size_t)count * N * 8, st));
+    rc = make_shat(c, sk_rlwe, shat, st);
+    int k = kind == FDFB_KEY_BRK ? 1 : (kind == FDFB_KEY_BPK ? 2 : 3);
+    if (!rc) rc = rlwe_entries(c, seed, k, sk_lwe, sk_rlwe, didx, 0, count, out, shat, tm, tp, st);
+    cudaFreeAsync(shat, st); cudaFreeAsync(tm, st); cudaFreeAsync(tp, st);
+  } else {
+    rc = FDFB_E_KIND;
+  }
+  cudaFreeAsync(didx, st);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(st));
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_key_import(const fdfb_ctx* c, int kind, const uint64_t* canon, void* dev_key, void* stream) {
+  if (!c || !canon || !dev_key) return FDFB_E_NULL;
+  cudaStream_t st = S(stream);
+  const fdfb_params& p = c->prm;
+  fdfb_sizes_t sz;
+  fdfb_sizes(c, &sz);
+  int rc = FDFB_OK;
+  if (kind == FDFB_KEY_BRK) {
+    size_t rows = brk_words(p) / (2 * (size_t)p.N);
+    const size_t CH = 4096;
+    u64* tmp;
+    CK(cudaMallocAsync(&tmp, CH * 2 * p.N * 8, st));
+    for (size_t o = 0; o < rows && !rc; o += CH) {
+      size_t cnt = (rows - o) < CH ? (rows - o) : CH;
+      rc = brk_import_rows(c, canon + o * 2 * p.N, cnt, o, (u64*)dev_key, tmp, st);
+    }
+    cudaFreeAsync(tmp, st);
+  } else if (kind == FDFB_KEY_BPK) {
+    CK(cudaMemcpyAsync(dev_key, canon, sz.bpk, cudaMemcpyDeviceToDevice, st));
+  } else if (kind == FDFB_KEY_KSK) {
+    CK(cudaMemcpyAsync(dev_key, canon, sz.ksk, cudaMemcpyDeviceToDevice, st));
+  } else if (kind == FDFB_KEY_PACK) {
+    rc = pack_import(c, canon, dev_key, st);
+  } else {
+    return FDFB_E_KIND;
+  }
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(st));
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_lwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_lwe, const uint64_t* msg,
+                                uint32_t count, uint32_t flags, uint64_t* out, void* stream) {
+  if (!c || !sk_lwe || !msg || !out) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;
+  k_lwe_encrypt<<<((size_t)count * 32 + 255) / 256, 256, 0, S(stream)>>>(c->dp, seed, sk_lwe, msg, count, flags, out);
+  CKL(c);
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_rlwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_rlwe, const uint64_t* msg,
+                                 uint32_t count, uint64_t* out, void* stream) {
+  if (!c || !sk_rlwe || !msg || !out) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;
+  cudaStream_t st = S(stream);
+  const int N = c->prm.N;
+  u64 *shat, *tm, *tp;
+  CK(cudaMallocAsync(&shat, (size_t)N * 8, st));
+  CK(cudaMallocAsync(&tm, (size_t)count * N * 8, st));
+  CK(cudaMallocAsync(&tp, (size_t)count * N * 8, st));
+  int rc = make_shat(c, sk_rlwe, shat, st);
+  dim3 g1((N + 255) / 256, count);
+  if (!rc) {
+    k_rlwe_enc_mask<<<g1, 256, 0, st>>>(c->dp, seed, count, tm);
+    CKL(c);
+    CK(cudaMemcpyAsync(tp, tm, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
+    rc = launch_ntt_batch(c, tp, count, 0, st);
+  }
+  if (!rc) {
+    size_t tot = (size_t)count * N;
+    k_pointwise_mul<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(tp, shat, tp, tot, N, c->dp.Q, c->qinv_neg, c->r2);
+    CKL(c);
+    rc = launch_ntt_batch(c, tp, count, 1, st);
+  }
+  if (!rc) {
+    k_rlwe_enc_finish<<<g1, 256, 0, st>>>(c->dp, seed, count, msg, tm, tp, out);
+    CKL(c);
+  }
+  cudaFreeAsync(shat, st); cudaFreeAsync(tm, st); cudaFreeAsync(tp, st);
+  return rc;
+}
+
+// ------------------------------------------------------------------ LUT
+extern "C" int fdfb_setup_lut(const fdfb_ctx* c, const uint64_t* lut, uint32_t t_out, uint64_t* rotp, void* stream) {
+  if (!c || !lut || !rotp) return FDFB_E_NULL;
+  if (t_out == 0) return FDFB_E_PLAINTEXT;
+  const fdfb_params& p = c->prm;
+  const u64 Q = p.Q;
+  const long long N = p.N, t = p.t;
+  const u64 delta = (u64)(((u128)2 * Q + t_out) / (2 * (u128)t_out));      // round(Q / t')
+  std::vector<u64> h(2 * N, 0);
+  // closed form of the half-open-window SetupPolynomial (reading F6): every y in [0,2N)
+  // is the y of exactly one (m, e); m(y) = floor((t y + N) / 2N) mod t.
+  for (long long y = 0; y < 2 * N; y++) {
+    long long m = ((t * y + N) / (2 * N)) % t;
+    u64 v = h_mulmod(delta, lut[m] % t_out, Q);
+    u64 nv = v ? Q - v : 0;
+    if (y == 0) h[0] = v;
+    else if (y < N) h[N - y] = nv;
+    else if (y == N) h[N] = nv;
+    else h[N + 2 * N - y] = v;
+  }
+  CK(cudaMemcpyAsync(rotp, h.data(), 2 * N * 8, cudaMemcpyHostToDevice, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  return FDFB_OK;
+}
+
+// ------------------------------------------------------------------ hot path
+extern "C" int fdfb_blind_rotate(const fdfb_ctx* c, const void* brk, uint64_t* acc, const uint32_t* abar,
+                                 uint32_t count, uint32_t acc_per_ct, void* stream) {
+  if (!c || !brk || !acc || !abar) return FDFB_E_NULL;
+  if (acc_per_ct == 0) return FDFB_E_DIMENSION;
+  return launch_br(c, (const u64*)brk, acc, (int)count, (int)acc_per_ct, abar, S(stream));
+}
+
+static int keyswitch_rlwe(const fdfb_ctx* c, const u64* bpk, const u64* lwe, int count, u64* out, cudaStream_t st) {
+  dim3 grd((2 * c->prm.N) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
+  k_keyswitch_rlwe<<<grd, KS_COLS, 0, st>>>(c->dp, bpk, lwe, count, out);
+  CKL(c);
+  return FDFB_OK;
+}
+static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int count, u64* out, cudaStream_t st) {
+  dim3 grd((c->prm.n + 1 + KS_COLS - 1) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
+  k_keyswitch_lwe<<<grd, KS_COLS, 0, st>>>(c->dp, ksk, lwe, count, out);
+  CKL(c);
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
+                                    const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
+                                    void* workspace, void* stream) {
+  if (!c || !brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;
+  cudaStream_t st = S(stream);
+  const fdfb_params& p = c->prm;
+  const int N = p.N, ellb = p.ell_boot;
+  BootWs w = boot_ws(p, B, workspace);
+  int rc;
+  size_t tot;
+  // 1. ModSwitch(ct, q_lwe, 2N)
+  tot = (size_t)B * (p.n + 1);
+  k_modswitch_in<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct_in, B, w.abar, w.bbar);
+  CKL(c);
+  // 2. ladder accumulators (reading R1)
+  tot = (size_t)B * ellb * N;
+  k_ladder_init<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.bbar, B, w.accs);
+  CKL(c);
+  // 3. ell_boot blind rotations of every ciphertext, batched
+  if ((rc = launch_br(c, (const u64*)brk, w.accs, (int)(B * ellb), ellb, w.abar, st))) return rc;
+  // 4. SampleExt(., 1) + L^{i-1}/2
+  tot = (size_t)B * ellb * (N + 1);
+  k_ladder_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.accs, B * ellb, w.lweN);
+  CKL(c);
+  // 5. BuildAcc: KeySwitch LWE->RLWE (into accs), PubMux
+  if ((rc = keyswitch_rlwe(c, (const u64*)bpk, w.lweN, (int)(B * ellb), w.accs, st))) return rc;
+  tot = (size_t)B * N;
+  k_pubmux_digits<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, B, w.dig);
+  CKL(c);
+  if ((rc = launch_ntt_batch(c, w.dig, (size_t)B * ellb, 0, st))) return rc;
+  if ((rc = launch_ntt_batch(c, w.accs, (size_t)B * ellb * 2, 0, st))) return rc;
+  tot = (size_t)B * 2 * N;
+  k_pubmux_mac<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.dig, w.accs, B, w.F, c->qinv_neg, c->r2);
+  CKL(c);
+  if ((rc = launch_ntt_batch(c, w.F, (size_t)B * 2, 1, st))) return rc;
+  tot = (size_t)B * N;
+  k_pubmux_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, B, w.F);
+  CKL(c);
+  // 6. final blind rotation
+  if ((rc = launch_br(c, (const u64*)brk, w.F, (int)B, 1, w.abar, st))) return rc;
+  // 7. SampleExt(., 1), ModSwitch(Q -> q_lwe), KeySwitch mod q_lwe (reading c.3)
+  tot = (size_t)B * (N + 1);
+  k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.F, B, w.lweN);
+  CKL(c);
+  return keyswitch_lwe(c, (const u64*)ksk, w.lweN, (int)B, ct_out, st);
+}
+
+extern "C" int fdfb_bootstrap_batch_host(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
+                                         const uint64_t* rotp, const uint64_t* in_h, uint64_t* out_h, uint32_t B,
+                                         void* workspace, void* stream) {
+  if (!c || !in_h || !out_h || !workspace) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;
+  cudaStream_t st = S(stream);
+  size_t bytes = (size_t)B * (c->prm.n + 1) * 8;
+  BootWs w = boot_ws(c->prm, B, workspace);
+  u64* din = (u64*)((char*)workspace + w.bytes);
+  u64* dout = din + (size_t)B * (c->prm.n + 1);
+  CK(cudaMemcpyAsync(din, in_h, bytes, cudaMemcpyHostToDevice, st));
+  int rc = fdfb_bootstrap_batch(c, brk, bpk, ksk, rotp, din, dout, B, workspace, stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out_h, dout, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_sample_extract(const fdfb_ctx* c, const uint64_t* rlwe, const uint32_t* k, uint64_t* lwe,
+                                   uint32_t B, void* stream) {
+  if (!c || !rlwe || !k || !lwe) return FDFB_E_NULL;
+  if (!B) return FDFB_OK;
+  size_t tot = (size_t)B * (c->prm.N + 1);
+  k_sample_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, S(stream)>>>(c->dp, rlwe, k, B, lwe);
+  CKL(c);
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_lwe_keyswitch(const fdfb_ctx* c, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
+                                  uint32_t B, void* stream) {
+  if (!c || !ksk || !lwe_N || !lwe_n) return FDFB_E_NULL;
+  if (!B) return FDFB_OK;
+  return keyswitch_lwe(c, (const u64*)ksk, lwe_N, (int)B, lwe_n, S(stream));
+}
+
+extern "C" int fdfb_poly_mul(const fdfb_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
+                             void* stream) {
+  if (!c || !a || !b || !out) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;
+  cudaStream_t st = S(stream);
+  const int N = c->prm.N;
+  u64* tb;
+  CK(cudaMallocAsync(&tb, (size_t)count * N * 8, st));
+  CK(cudaMemcpyAsync(out, a, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(tb, b, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
+  int rc = launch_ntt_batch(c, out, count, 0, st);
+  if (!rc) rc = launch_ntt_batch(c, tb, count, 0, st);
+  if (!rc) {
+    size_t tot = (size_t)count * N;
+    k_pointwise_mul<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(out, tb, out, tot, tot, c->dp.Q, c->qinv_neg, c->r2);
+    CKL(c);
+    rc = launch_ntt_batch(c, out, count, 1, st);
+  }
+  cudaFreeAsync(tb, st);
+  return rc;
+}
+
+extern "C" int fdfb_cdt_table(const fdfb_ctx* c, uint64_t* thr, int* T) {
+  if (!c || !T) return FDFB_E_NULL;
+  *T = c->dp.cdt_T;
+  if (thr) for (size_t i = 0; i < c->cdt.size(); i++) thr[i] = c->cdt[i];
+  return FDFB_OK;
+}
+extern "C" uint64_t fdfb_launch_count(const fdfb_ctx* c) { return c ? (uint64_t)c->launches.load() : 0; }
+
+extern "C" const char* fdfb_status_string(int s) {
+  switch (s) {
+    case FDFB_OK: return "ok";
+    case FDFB_E_NULL: return "null pointer argument";
+    case FDFB_E_NON_NTT_MODULUS: return "Q is not a prime with Q = 1 mod 2N (or Q >= 2^56)";
+    case FDFB_E_DIMENSION: return "dimension out of range";
+    case FDFB_E_DECOMP: return "gadget decomposition: ell != ceil(bits / logL) or out of range";
+    case FDFB_E_INDEX: return "index out of range";
+    case FDFB_E_PLAINTEXT: return "plaintext modulus t must divide 2N";
+    case FDFB_E_UNSUPPORTED: return "unsupported parameter combination";
+    case FDFB_E_CUDA: return "CUDA error";
+    case FDFB_E_WORKSPACE: return "workspace too small";
+    case FDFB_E_KIND: return "unknown key kind";
+  }
+  return "unknown status";
+}
+extern "C" const char* fdfb_last_cuda_error(void) { return g_last_cuda.c_str(); }
+#include "shift_host.inc"

@@ -1,0 +1,348 @@
+// kernels_boot.cuh -- the FDFB bootstrap hot path (Fig. Bootstrap).
+#pragma once
+#include "kernels_core.cuh"
+
+// ---------------------------------------------------------------------------
+// a1: ModSwitch(ct, q_lwe, 2N) -- round half up.
+// q_lwe = 2^w, 2N = 2^{logN+1}: round(2N x / q) = ((x >> (w - logN - 2)) + 1) >> 1.
+__global__ void k_modswitch_in(DevParams p, const u64* __restrict__ ct, int B, u32* __restrict__ abar,
+                               u32* __restrict__ bbar) {
+  const int sh = p.log_q_lwe - (p.logN + 1) - 1;
+  const u32 m2N = 2 * p.N - 1;
+  size_t total = (size_t)B * (p.n + 1);
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    size_t c = x / (p.n + 1); int i = (int)(x % (p.n + 1));
+    u64 v = ct[x] & p.q_mask;
+    u32 r = (u32)(((v >> sh) + 1) >> 1) & m2N;
+    if (i == 0) bbar[c] = r; else abar[c * p.n + (i - 1)] = r;
+  }
+}
+
+// a2: ladder accumulators acc_{c,i} = [L_boot^{i} 2^{-1} sgnP X^{bbar_c}, 0]  (reading R1),
+// sgnP = 1 - sum_{i>=1} X^i.
+__global__ void k_ladder_init(DevParams p, const u32* __restrict__ bbar, int B, u64* __restrict__ accs) {
+  const int N = p.N, ell = p.ell_boot;
+  size_t total = (size_t)B * ell * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    size_t g = x / N; int j = (int)(x % N);
+    int c = (int)(g / ell), i = (int)(g % ell);
+    u64 cst = mul_mod_slow(pow2_mod(p.logL_boot * i, p.Q), p.half, p.Q);
+    // coefficient j of sgnP * X^{bbar}: e = (j - bbar) mod 2N; sgnP[e] for e<N, -sgnP[e-N] else
+    int e = (j - (int)bbar[c]) & (2 * N - 1);
+    int sgn = (e == 0) ? 1 : (e < N ? -1 : (e == N ? -1 : 1));
+    u64* acc = accs + g * 2 * N;
+    acc[j] = sgn > 0 ? cst : neg_mod(cst, p.Q);
+    acc[N + j] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a3: batched blind rotation.  Persistent CTAs of N/8 threads;
+// each CTA keeps ONE accumulator resident in shared memory for all n*u CMux steps
+// and streams brK[i,j] (shared by every accumulator of the batch, L2-resident per
+// step) once per step.  One CMux step:
+//   d = acc X^e - acc (canonical), e = -abar_i u_j mod 2N
+//   for each of the 2*ell digit polynomials D_r = Decomp_{L,Q}(d)[r]:
+//       NTT(D_r) (registers + swizzled smem), MAC with brK[i,j][r] (Shoup, [0,2Q))
+//   acc += INTT(MAC) (N^{-1} folded into brK).
+template <int N>
+__global__ void __launch_bounds__(N / 8)
+k_blind_rotate(DevParams p, const u64* __restrict__ bsk, u64* __restrict__ accs, int n_acc, int acc_per_ct,
+               const u32* __restrict__ abar) {
+  constexpr int T = N / 8;
+  extern __shared__ u64 smem[];
+  u64* sacc = smem;            // [b | a], natural order, canonical
+  u64* sb0 = smem + 2 * N;     // NTT exchange buffers (double-buffered)
+  u64* sb1 = smem + 3 * N;
+  const int tid = threadIdx.x;
+  const u64 Q = p.Q, Q2 = p.Q2;
+  const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
+  const u64 dmask = (1ULL << logL) - 1;
+  const size_t step_stride = (size_t)2 * ell * 4 * N;
+
+  for (int g = blockIdx.x; g < n_acc; g += gridDim.x) {
+    u64* acc = accs + (size_t)g * 2 * N;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
+    const u32* ab = abar + (size_t)(g / acc_per_ct) * p.n;
+    for (int i = 0; i < p.n; i++) {
+      const u32 ai = __ldg(ab + i);
+      for (int j = 0; j < u; j++) {
+        // exponent -abar_i * u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
+        const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
+        const u64* K = bsk + ((size_t)i * u + j) * step_stride;
+        __syncthreads();                                   // previous step's acc writes
+        u64 mb[8], ma[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
+        int buf = 0;
+#pragma unroll 1
+        for (int half = 0; half < 2; half++) {
+          const u64* src = sacc + half * N;
+          u64 d[8];
+#pragma unroll
+          for (int k = 0; k < 8; k++) {
+            const int pos = tid + T * k;
+            d[k] = sub_mod(rot_coeff(src, pos, e, N, Q), src[pos], Q);
+          }
+#pragma unroll 1
+          for (int r = 0; r < ell; r++) {
+            u64 x[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) x[k] = (d[k] >> (r * logL)) & dmask;
+            ntt_fwd<N>(x, buf ? sb1 : sb0, tid, p);
+            buf ^= 1;
+            const u64* Kr = K + (size_t)(half * ell + r) * 4 * N + 8 * tid;
+            const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(Kr);
+            const ulonglong2* kbp = reinterpret_cast<const ulonglong2*>(Kr + N);
+            const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(Kr + 2 * N);
+            const ulonglong2* kap = reinterpret_cast<const ulonglong2*>(Kr + 3 * N);
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+              ulonglong2 w = __ldg(kb + v), wp = __ldg(kbp + v);
+              mb[2 * v] += mul_shoup_lazy(x[2 * v], w.x, wp.x, Q);
+              mb[2 * v + 1] += mul_shoup_lazy(x[2 * v + 1], w.y, wp.y, Q);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+              ulonglong2 w = __ldg(ka + v), wp = __ldg(kap + v);
+              ma[2 * v] += mul_shoup_lazy(x[2 * v], w.x, wp.x, Q);
+              ma[2 * v + 1] += mul_shoup_lazy(x[2 * v + 1], w.y, wp.y, Q);
+            }
+          }
+        }
+        // sums of 2*ell terms in [0, 2Q): reduce into [0, 2Q) for the inverse transform
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          u64 vb = mb[k], va = ma[k];
+#pragma unroll
+          for (int s = 4; s >= 1; s--) { vb = csub(vb, Q << s); va = csub(va, Q << s); }
+          mb[k] = vb; ma[k] = va;
+        }
+        ntt_inv<N>(mb, buf ? sb1 : sb0, tid, p);
+        buf ^= 1;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int pos = tid + T * k;
+          sacc[pos] = add_mod(sacc[pos], csub(mb[k], Q), Q);
+        }
+        ntt_inv<N>(ma, buf ? sb1 : sb0, tid, p);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int pos = N + tid + T * k;
+          sacc[pos] = add_mod(sacc[pos], csub(ma[k], Q), Q);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a4: ladder SampleExt(acc, 1) + [L_boot^{i} 2^{-1}, 0]
+// -> LWE_N mod Q:  b' = b_0,  a'_0 = a_0,  a'_I = -a_{N-I} (I >= 1; NSgn(0) = -1).
+__global__ void k_ladder_extract(DevParams p, const u64* __restrict__ accs, int count, u64* __restrict__ lwe) {
+  const int N = p.N;
+  size_t total = (size_t)count * (N + 1);
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    size_t g = x / (N + 1); int I = (int)(x % (N + 1));
+    const u64* acc = accs + g * 2 * N;
+    u64 v;
+    if (I == 0) {
+      int i = (int)(g % p.ell_boot);
+      u64 cst = mul_mod_slow(pow2_mod(p.logL_boot * i, p.Q), p.half, p.Q);
+      v = add_mod(acc[0], cst, p.Q);
+    } else {
+      int a = I - 1;
+      v = (a == 0) ? acc[N] : neg_mod(acc[N + N - a], p.Q);
+    }
+    lwe[x] = v;
+  }
+}
+
+// a6 (first half): c_Q = SampleExt(acc_F, 1), then ModSwitch(Q -> q_lwe) per coefficient:
+// floor((2 q x + Q) / (2Q)) mod q  (reading c.3 order, round half up).
+__global__ void k_extract_modswitch(DevParams p, const u64* __restrict__ accs, int count, u64* __restrict__ lwe) {
+  const int N = p.N;
+  size_t total = (size_t)count * (N + 1);
+  const unsigned __int128 twoQ = (unsigned __int128)2 * p.Q;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    size_t g = x / (N + 1); int I = (int)(x % (N + 1));
+    const u64* acc = accs + g * 2 * N;
+    u64 v;
+    if (I == 0) v = acc[0];
+    else { int a = I - 1; v = (a == 0) ? acc[N] : neg_mod(acc[N + N - a], p.Q); }
+    unsigned __int128 num = ((unsigned __int128)v << (p.log_q_lwe + 1)) + p.Q;
+    lwe[x] = (u64)(num / twoQ) & p.q_mask;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a5 (KeySwitch LWE_N -> RLWE with bpK), batched as a
+// digit-matrix x key-matrix product:  out[g] = [b_g, 0] - sum_{i,j} Decomp(a_{g,i})[j] * bpK[i,j].
+// CTA tile: KS_ROWS ciphertexts x KS_COLS output coefficients (of 2N).  Exact
+// accumulation: key split in 32-bit halves, digit (< 2^logL) x half accumulated
+// in u64 (no overflow for N*ell*2^logL*2^32 < 2^64), reduced mod Q at the end.
+#define KS_ROWS 16
+#define KS_COLS 128
+__global__ void __launch_bounds__(KS_COLS)
+k_keyswitch_rlwe(DevParams p, const u64* __restrict__ bpk, const u64* __restrict__ lwe, int count,
+                 u64* __restrict__ out) {
+  const int N = p.N, ell = p.ell_pk, logL = p.logL_pk;
+  const u64 Q = p.Q, dmask = (1ULL << logL) - 1;
+  const int col = blockIdx.x * KS_COLS + threadIdx.x;   // in [0, 2N)
+  const int row0 = blockIdx.y * KS_ROWS;
+  __shared__ u64 sa[KS_ROWS][33];
+  u64 lo[KS_ROWS], hi[KS_ROWS];
+#pragma unroll
+  for (int r = 0; r < KS_ROWS; r++) { lo[r] = 0; hi[r] = 0; }
+  for (int i0 = 0; i0 < N; i0 += 32) {
+    __syncthreads();
+    for (int x = threadIdx.x; x < KS_ROWS * 32; x += KS_COLS) {
+      int r = x / 32, ii = x % 32;
+      int g = row0 + r;
+      sa[r][ii] = (g < count && i0 + ii < N) ? lwe[(size_t)g * (N + 1) + 1 + i0 + ii] : 0;
+    }
+    __syncthreads();
+    for (int ii = 0; ii < 32 && i0 + ii < N; ii++) {
+      const u64* krow = bpk + ((size_t)(i0 + ii) * ell) * 2 * N + col;
+      for (int j = 0; j < ell; j++) {
+        u64 kv = __ldg(krow + (size_t)j * 2 * N);
+        u32 klo = (u32)kv, khi = (u32)(kv >> 32);
+#pragma unroll
+        for (int r = 0; r < KS_ROWS; r++) {
+          u32 dg = (u32)((sa[r][ii] >> (j * logL)) & dmask);
+          lo[r] += (u64)dg * klo;
+          hi[r] += (u64)dg * khi;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < KS_ROWS; r++) {
+    int g = row0 + r;
+    if (g >= count) continue;
+    unsigned __int128 s = ((unsigned __int128)hi[r] << 32) + lo[r];
+    u64 v = neg_mod((u64)(s % Q), Q);
+    if (col == 0) v = add_mod(v, lwe[(size_t)g * (N + 1)], Q);
+    out[(size_t)g * 2 * N + col] = v;
+  }
+}
+
+// a6 (second half): LWE KeySwitch N -> n mod q_lwe, same tiling;
+// arithmetic mod 2^w is native u64 wrap.
+__global__ void __launch_bounds__(KS_COLS)
+k_keyswitch_lwe(DevParams p, const u64* __restrict__ ksk, const u64* __restrict__ lwe, int count,
+                u64* __restrict__ out) {
+  const int N = p.N, n = p.n, ell = p.ell_ks, logL = p.logL_ks;
+  const u64 dmask = (1ULL << logL) - 1;
+  const int col = blockIdx.x * KS_COLS + threadIdx.x;   // in [0, n+1)
+  const int row0 = blockIdx.y * KS_ROWS;
+  const bool act = col <= n;
+  __shared__ u64 sa[KS_ROWS][33];
+  u64 acc[KS_ROWS];
+#pragma unroll
+  for (int r = 0; r < KS_ROWS; r++) acc[r] = 0;
+  for (int i0 = 0; i0 < N; i0 += 32) {
+    __syncthreads();
+    for (int x = threadIdx.x; x < KS_ROWS * 32; x += KS_COLS) {
+      int r = x / 32, ii = x % 32;
+      int g = row0 + r;
+      sa[r][ii] = (g < count && i0 + ii < N) ? lwe[(size_t)g * (N + 1) + 1 + i0 + ii] : 0;
+    }
+    __syncthreads();
+    if (act) {
+      for (int ii = 0; ii < 32 && i0 + ii < N; ii++) {
+        const u64* krow = ksk + ((size_t)(i0 + ii) * ell) * (n + 1) + col;
+        for (int j = 0; j < ell; j++) {
+          u64 kv = __ldg(krow + (size_t)j * (n + 1));
+#pragma unroll
+          for (int r = 0; r < KS_ROWS; r++) {
+            u64 dg = (sa[r][ii] >> (j * logL)) & dmask;
+            acc[r] += dg * kv;
+          }
+        }
+      }
+    }
+  }
+  if (!act) return;
+#pragma unroll
+  for (int r = 0; r < KS_ROWS; r++) {
+    int g = row0 + r;
+    if (g >= count) continue;
+    u64 v = (col == 0 ? lwe[(size_t)g * (N + 1)] : 0) - acc[r];
+    out[(size_t)g * (n + 1) + col] = v & p.q_mask;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a5 (PubMux, readings R1 + F4): per ciphertext c,
+//   r_x = rotP_x X^{bbar_c};  p0 := r_1, p1 := r_0 (swap);  P = Decomp_{L_boot}(p1 - p0)
+//   acc_F = [p0, 0] + sum_i P[i] * acc_{R,c,i}   (ring products via NTT, Montgomery MAC).
+// Step 1: digit polynomials (coef domain) into dig[c][i][N]; accR NTT'd in place by k_ntt_batch.
+__global__ void k_pubmux_digits(DevParams p, const u64* __restrict__ rotp, const u32* __restrict__ bbar, int B,
+                                u64* __restrict__ dig) {
+  const int N = p.N, ell = p.ell_boot, logL = p.logL_boot;
+  const u64 dmask = (1ULL << logL) - 1, Q = p.Q;
+  size_t total = (size_t)B * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    int c = (int)(x / N), j = (int)(x % N);
+    int e = (int)bbar[c];
+    u64 r0 = rot_coeff(rotp, j, e, N, Q), r1 = rot_coeff(rotp + N, j, e, N, Q);
+    u64 pd = sub_mod(r0, r1, Q);                        // p1 - p0 = r0 - r1
+    for (int i = 0; i < ell; i++) dig[((size_t)c * ell + i) * N + j] = (pd >> (i * logL)) & dmask;
+  }
+}
+// Step 2 (NTT domain): F[c][col] = sum_i Dhat[c][i] * Ahat[c][i][col]
+__global__ void k_pubmux_mac(DevParams p, const u64* __restrict__ dig_hat, const u64* __restrict__ accR_hat, int B,
+                             u64* __restrict__ F, u64 qinv_neg, u64 r2) {
+  const int N = p.N, ell = p.ell_boot;
+  const u64 Q = p.Q;
+  size_t total = (size_t)B * 2 * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    int c = (int)(x / (2 * N)); int cs = (int)(x % (2 * N)); int col = cs / N, s = cs % N;
+    u64 acc = 0;
+    for (int i = 0; i < ell; i++) {
+      u64 dv = dig_hat[((size_t)c * ell + i) * N + s];
+      u64 av = accR_hat[(((size_t)c * ell + i) * 2 + col) * N + s];
+      acc = add_mod(acc, csub(mont_mul(dv, av, Q, qinv_neg), Q), Q);
+    }
+    F[x] = csub(mont_mul(acc, r2, Q, qinv_neg), Q);
+  }
+}
+// Step 3 (after inverse NTT of F): acc_F = [p0, 0] + F, p0 = rotP_1 X^{bbar}
+__global__ void k_pubmux_finish(DevParams p, const u64* __restrict__ rotp, const u32* __restrict__ bbar, int B,
+                                u64* __restrict__ F) {
+  const int N = p.N;
+  size_t total = (size_t)B * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    int c = (int)(x / N), j = (int)(x % N);
+    u64 r1 = rot_coeff(rotp + N, j, (int)bbar[c], N, p.Q);
+    u64* f = F + (size_t)c * 2 * N;
+    f[j] = add_mod(f[j], r1, p.Q);
+  }
+}
+
+// Standalone SampleExt with per-item 1-based k.
+__global__ void k_sample_extract(DevParams p, const u64* __restrict__ rlwe, const u32* __restrict__ kk, int B,
+                                 u64* __restrict__ lwe) {
+  const int N = p.N;
+  size_t total = (size_t)B * (N + 1);
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    size_t g = x / (N + 1); int I = (int)(x % (N + 1));
+    const u64* ct = rlwe + g * 2 * N;
+    int k = (int)kk[g];                      // 1-based
+    u64 v;
+    if (I == 0) v = ct[k - 1];
+    else {
+      int i = I;                             // 1-based i
+      int idx = ((k - i) % N + N) % N;
+      u64 a = ct[N + idx];
+      v = (k - i + 1 > 0) ? a : neg_mod(a, p.Q);
+    }
+    lwe[x] = v;
+  }
+}

@@ -1,0 +1,275 @@
+"""Thin ctypes binding of libfdfb.so (include/fdfb.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+libfdfb.so.  torch is used for device memory and streams.  There is NO CPU
+fallback: if the shared library is missing or no CUDA device is present the
+calls raise.
+"""
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfdfb.so")
+
+KEY_BRK, KEY_BPK, KEY_KSK, KEY_PACK, KEY_SK_LWE, KEY_SK_RLWE = 1, 2, 3, 4, 5, 6
+
+
+class fdfb_params(C.Structure):
+    _fields_ = [("N", C.c_uint32), ("n", C.c_uint32), ("Q", C.c_uint64), ("log_q_lwe", C.c_uint32),
+                ("lwe_key", C.c_uint32), ("rlwe_key", C.c_uint32),
+                ("logL_rgsw", C.c_uint32), ("ell_rgsw", C.c_uint32), ("logL_boot", C.c_uint32),
+                ("ell_boot", C.c_uint32), ("logL_pk", C.c_uint32), ("ell_pk", C.c_uint32),
+                ("logL_ks", C.c_uint32), ("ell_ks", C.c_uint32), ("logL_pack", C.c_uint32),
+                ("ell_pack", C.c_uint32), ("t", C.c_uint32), ("sigma_milli", C.c_uint32)]
+
+
+class fdfb_sizes_t(C.Structure):
+    _fields_ = [(k, C.c_size_t) for k in ("sk_lwe", "sk_rlwe", "brk", "bpk", "ksk", "pack",
+                                           "canon_brk", "canon_bpk", "canon_ksk", "canon_pack")]
+
+
+class FdfbError(RuntimeError):
+    pass
+
+
+_lib = None
+_EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace_bootstrap", "fdfb_workspace_shift",
+            "fdfb_workspace_vector_pack", "fdfb_keygen", "fdfb_keygen_canonical", "fdfb_key_import",
+            "fdfb_lwe_encrypt", "fdfb_rlwe_encrypt", "fdfb_setup_lut", "fdfb_bootstrap_batch",
+            "fdfb_bootstrap_batch_host", "fdfb_blind_rotate", "fdfb_sample_extract", "fdfb_lwe_keyswitch",
+            "fdfb_vector_pack", "fdfb_shift", "fdfb_poly_mul", "fdfb_cdt_table", "fdfb_launch_count",
+            "fdfb_status_string", "fdfb_last_cuda_error"]
+
+
+def lib():
+    """Load libfdfb.so (no fallback: raises if absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FdfbError("libfdfb.so not built (run __graft_entry__.build()); no CPU fallback exists")
+        L = C.CDLL(LIB_PATH)
+        vp, u32, u64, sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_size_t
+        L.fdfb_ctx_create.argtypes = [C.POINTER(fdfb_params), C.c_int, C.POINTER(vp)]
+        L.fdfb_ctx_destroy.argtypes = [vp]
+        L.fdfb_ctx_destroy.restype = None
+        L.fdfb_sizes.argtypes = [vp, C.POINTER(fdfb_sizes_t)]
+        L.fdfb_workspace_bootstrap.argtypes = [vp, u32]
+        L.fdfb_workspace_bootstrap.restype = sz
+        L.fdfb_workspace_shift.argtypes = [vp, u32]
+        L.fdfb_workspace_shift.restype = sz
+        L.fdfb_workspace_vector_pack.argtypes = [vp, u32, u32]
+        L.fdfb_workspace_vector_pack.restype = sz
+        L.fdfb_keygen.argtypes = [vp, u64, u32, vp, vp, vp, vp, vp, vp, vp]
+        L.fdfb_keygen_canonical.argtypes = [vp, u64, C.c_int, vp, vp, vp, u32, vp, vp]
+        L.fdfb_key_import.argtypes = [vp, C.c_int, vp, vp, vp]
+        L.fdfb_lwe_encrypt.argtypes = [vp, u64, vp, vp, u32, u32, vp, vp]
+        L.fdfb_rlwe_encrypt.argtypes = [vp, u64, vp, vp, u32, vp, vp]
+        L.fdfb_setup_lut.argtypes = [vp, vp, u32, vp, vp]
+        L.fdfb_bootstrap_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_bootstrap_batch_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_blind_rotate.argtypes = [vp, vp, vp, vp, u32, u32, vp]
+        L.fdfb_sample_extract.argtypes = [vp, vp, vp, vp, u32, vp]
+        L.fdfb_lwe_keyswitch.argtypes = [vp, vp, vp, vp, u32, vp]
+        L.fdfb_vector_pack.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
+        L.fdfb_shift.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_poly_mul.argtypes = [vp, vp, vp, vp, u32, vp]
+        L.fdfb_cdt_table.argtypes = [vp, vp, C.POINTER(C.c_int)]
+        L.fdfb_launch_count.argtypes = [vp]
+        L.fdfb_launch_count.restype = u64
+        L.fdfb_status_string.argtypes = [C.c_int]
+        L.fdfb_status_string.restype = C.c_char_p
+        L.fdfb_last_cuda_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        L = lib()
+        msg = L.fdfb_status_string(rc).decode()
+        if rc == -8:
+            msg += ": " + L.fdfb_last_cuda_error().decode()
+        raise FdfbError("fdfb error %d: %s" % (rc, msg))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise FdfbError("tensor must be contiguous")
+        return C.c_void_p(t.data_ptr())
+    return t
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def params_from_config(cfg: dict, noiseless: bool = False) -> fdfb_params:
+    p = fdfb_params()
+    for k in ("N", "n", "Q", "log_q_lwe", "logL_rgsw", "ell_rgsw", "logL_boot", "ell_boot", "logL_pk", "ell_pk",
+              "logL_ks", "ell_ks", "logL_pack", "ell_pack", "t"):
+        setattr(p, k, int(cfg[k]))
+    p.lwe_key = 1 if cfg["lwe_key"] == "ternary" else 0
+    p.rlwe_key = 1 if cfg["rlwe_key"] == "ternary" else 0
+    p.sigma_milli = 0 if (noiseless or cfg.get("sigma", 3.2) == 0) else int(round(cfg.get("sigma", 3.2) * 1000))
+    return p
+
+
+class Context:
+    """One parameter set on one device.  Methods mirror the C-ABI names."""
+
+    def __init__(self, cfg: dict, device: int = 0, noiseless: bool = False):
+        if not torch.cuda.is_available():
+            raise FdfbError("no CUDA device: the FDFB library has no CPU path")
+        self.cfg = dict(cfg)
+        self.device = torch.device("cuda", device)
+        self.p = params_from_config(cfg, noiseless)
+        h = C.c_void_p()
+        _check(lib().fdfb_ctx_create(C.byref(self.p), device, C.byref(h)))
+        self.h = h
+        self.N, self.n, self.Q = cfg["N"], cfg["n"], cfg["Q"]
+        self.u = 2 if cfg["lwe_key"] == "ternary" else 1
+        s = fdfb_sizes_t()
+        _check(lib().fdfb_sizes(self.h, C.byref(s)))
+        self.sizes = {k: getattr(s, k) for k, _ in fdfb_sizes_t._fields_}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().fdfb_ctx_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- buffers
+    def _u64(self, *shape):
+        return torch.empty(shape, dtype=torch.uint64, device=self.device)
+
+    def _bytes(self, n):
+        return torch.empty(max(int(n), 8), dtype=torch.uint8, device=self.device)
+
+    def launch_count(self) -> int:
+        return int(lib().fdfb_launch_count(self.h))
+
+    # ---------------------------------------------------------------- keys
+    def keygen(self, seed: int, which: int = 0x0F, sk=None, stream=None):
+        """fdfb_keygen: returns dict of device tensors (secrets + opaque keys)."""
+        if sk is None:
+            sk = (torch.empty(self.n, dtype=torch.int8, device=self.device),
+                  torch.empty(self.N, dtype=torch.int8, device=self.device))
+            which |= 1
+        keys = {"s": sk[0], "S": sk[1]}
+        for bit, name in ((2, "brk"), (4, "bpk"), (8, "ksk"), (16, "pack")):
+            keys[name] = self._bytes(self.sizes[name]) if which & bit else None
+        _check(lib().fdfb_keygen(self.h, C.c_uint64(seed), which, _ptr(keys["s"]), _ptr(keys["S"]),
+                                 _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]), _ptr(keys["pack"]),
+                                 _stream(stream)))
+        return keys
+
+    def keygen_canonical(self, seed, kind, s, S, idx, stream=None):
+        import numpy as np
+        idx = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64))
+        per = (self.n + 1) if kind == KEY_KSK else 2 * self.N
+        out = self._u64(len(idx), per)
+        _check(lib().fdfb_keygen_canonical(self.h, C.c_uint64(seed), kind, _ptr(s), _ptr(S),
+                                           idx.ctypes.data_as(C.c_void_p), len(idx), _ptr(out), _stream(stream)))
+        return out
+
+    def key_import(self, kind: int, canonical: torch.Tensor, stream=None):
+        name = {KEY_BRK: "brk", KEY_BPK: "bpk", KEY_KSK: "ksk", KEY_PACK: "pack"}[kind]
+        dev = self._bytes(self.sizes[name])
+        _check(lib().fdfb_key_import(self.h, kind, _ptr(canonical.contiguous()), _ptr(dev), _stream(stream)))
+        return dev
+
+    # ---------------------------------------------------------------- inputs / LUT
+    def lwe_encrypt(self, seed, s, msgs: torch.Tensor, exact=False, stream=None):
+        out = self._u64(msgs.numel(), self.n + 1)
+        _check(lib().fdfb_lwe_encrypt(self.h, C.c_uint64(seed), _ptr(s), _ptr(msgs), msgs.numel(),
+                                      1 if exact else 0, _ptr(out), _stream(stream)))
+        return out
+
+    def rlwe_encrypt(self, seed, S, msgs: torch.Tensor, stream=None):
+        cnt = msgs.shape[0]
+        out = self._u64(cnt, 2, self.N)
+        _check(lib().fdfb_rlwe_encrypt(self.h, C.c_uint64(seed), _ptr(S), _ptr(msgs), cnt, _ptr(out),
+                                       _stream(stream)))
+        return out
+
+    def setup_lut(self, lut, t_out=None, stream=None):
+        import numpy as np
+        lut = np.ascontiguousarray(np.asarray(lut, dtype=np.uint64))
+        t_out = self.cfg["t"] if t_out is None else t_out
+        rotp = self._u64(2, self.N)
+        _check(lib().fdfb_setup_lut(self.h, lut.ctypes.data_as(C.c_void_p), t_out, _ptr(rotp), _stream(stream)))
+        return rotp
+
+    # ---------------------------------------------------------------- hot path
+    def workspace_bootstrap(self, B):
+        return self._bytes(lib().fdfb_workspace_bootstrap(self.h, B))
+
+    def bootstrap_batch(self, keys, rotp, ct_in, ct_out=None, workspace=None, stream=None):
+        B = ct_in.shape[0]
+        ct_out = self._u64(B, self.n + 1) if ct_out is None else ct_out
+        ws = self.workspace_bootstrap(B) if workspace is None else workspace
+        _check(lib().fdfb_bootstrap_batch(self.h, _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]),
+                                          _ptr(rotp), _ptr(ct_in), _ptr(ct_out), B, _ptr(ws), _stream(stream)))
+        return ct_out
+
+    def bootstrap_batch_host(self, keys, rotp, ct_in_host, ct_out_host, workspace, stream=None):
+        B = ct_in_host.shape[0]
+        _check(lib().fdfb_bootstrap_batch_host(self.h, _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]),
+                                               _ptr(rotp), _ptr(ct_in_host), _ptr(ct_out_host), B, _ptr(workspace),
+                                               _stream(stream)))
+        return ct_out_host
+
+    def blind_rotate(self, brk, acc, abar, acc_per_ct=1, stream=None):
+        _check(lib().fdfb_blind_rotate(self.h, _ptr(brk), _ptr(acc), _ptr(abar), acc.shape[0], acc_per_ct,
+                                       _stream(stream)))
+        return acc
+
+    def sample_extract(self, rlwe, k, stream=None):
+        B = rlwe.shape[0]
+        out = self._u64(B, self.N + 1)
+        _check(lib().fdfb_sample_extract(self.h, _ptr(rlwe), _ptr(k), _ptr(out), B, _stream(stream)))
+        return out
+
+    def lwe_keyswitch(self, ksk, lwe, stream=None):
+        B = lwe.shape[0]
+        out = self._u64(B, self.n + 1)
+        _check(lib().fdfb_lwe_keyswitch(self.h, _ptr(ksk), _ptr(lwe), _ptr(out), B, _stream(stream)))
+        return out
+
+    def vector_pack(self, pack, lwe, stream=None):
+        B, m = lwe.shape[0], lwe.shape[1]
+        out = self._u64(B, 2, self.N)
+        ws = self._bytes(lib().fdfb_workspace_vector_pack(self.h, m, B))
+        _check(lib().fdfb_vector_pack(self.h, _ptr(pack), _ptr(lwe), m, _ptr(out), B, _ptr(ws), _stream(stream)))
+        return out
+
+    def workspace_shift(self, B):
+        return self._bytes(lib().fdfb_workspace_shift(self.h, B))
+
+    def shift(self, pack, rlwe, d, out=None, workspace=None, stream=None):
+        B = rlwe.shape[0]
+        out = self._u64(B, 2, self.N) if out is None else out
+        ws = self.workspace_shift(B) if workspace is None else workspace
+        _check(lib().fdfb_shift(self.h, _ptr(pack), _ptr(rlwe), _ptr(d), _ptr(out), B, _ptr(ws), _stream(stream)))
+        return out
+
+    def poly_mul(self, a, b, stream=None):
+        out = torch.empty_like(a)
+        _check(lib().fdfb_poly_mul(self.h, _ptr(a), _ptr(b), _ptr(out), a.shape[0], _stream(stream)))
+        return out
+
+    def cdt_table(self):
+        import numpy as np
+        T = C.c_int()
+        _check(lib().fdfb_cdt_table(self.h, None, C.byref(T)))
+        out = np.zeros(2 * T.value, dtype=np.uint64)
+        _check(lib().fdfb_cdt_table(self.h, out.ctypes.data_as(C.c_void_p), C.byref(T)))
+        return out
