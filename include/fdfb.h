@@ -163,6 +163,14 @@ int fdfb_poly_mul(const fdfb_ctx* ctx, const uint64_t* a, const uint64_t* b, uin
                   void* stream);
 /* The library's own CDT thresholds (2T values) into thr [host]; *T = tail cut. */
 int fdfb_cdt_table(const fdfb_ctx* ctx, uint64_t* thr, int* T);
+/* Per-kernel-class timing for the roofline report: when enabled, every launch of the
+ * classes below is bracketed by CUDA events recorded on the launching stream.
+ * fdfb_timing_read waits for the recorded events of class `kclass`, returns their
+ * summed device time (ms) and launch count, and forgets them. */
+enum { FDFB_KCLASS_BLIND_ROTATE = 0, FDFB_KCLASS_KEYSWITCH_RLWE = 1, FDFB_KCLASS_KEYSWITCH_LWE = 2,
+       FDFB_KCLASS_SHIFT = 3 };
+int fdfb_timing_enable(const fdfb_ctx* ctx, int on);
+int fdfb_timing_read(const fdfb_ctx* ctx, int kclass, double* total_ms, uint64_t* launches);
 /* Number of kernel launches issued by this context so far (bench evidence). */
 uint64_t fdfb_launch_count(const fdfb_ctx* ctx);
 const char* fdfb_status_string(int status);

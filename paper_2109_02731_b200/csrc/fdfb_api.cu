@@ -26,6 +26,24 @@ struct fdfb_ctx {
   u64 omega_off;             // offset of NTT(X) slots (omega) in d_tables
   std::vector<u64> cdt;
   mutable std::atomic<unsigned long long> launches{0};
+  // optional per-kernel-class CUDA-event timing (fdfb_timing_enable / fdfb_timing_read)
+  mutable std::mutex tmu;
+  mutable bool timing = false;
+  mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
+};
+
+// Bracket one launch of kernel class `cls` with events on its stream when timing is on.
+struct TimedLaunch {
+  const fdfb_ctx* c; int cls; cudaStream_t st; cudaEvent_t e1 = nullptr;
+  TimedLaunch(const fdfb_ctx* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+    if (!c->timing) return;
+    cudaEvent_t e0;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    std::lock_guard<std::mutex> g(c->tmu);
+    c->tev.push_back({cls, {e0, e1}});
+  }
+  ~TimedLaunch() { if (e1) cudaEventRecord(e1, st); }
 };
 
 static thread_local std::string g_last_cuda;
@@ -158,6 +176,7 @@ static int launch_br_t(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, 
   if (per_sm < 1) per_sm = 1;
   int grid = c->num_sms * per_sm;
   if (grid > n_acc) grid = n_acc;
+  TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
   k_blind_rotate<N><<<grid, T, sm, st>>>(c->dp, bsk, accs, n_acc, acc_per_ct, abar);
   CKL(c);
   return FDFB_OK;
@@ -543,12 +562,14 @@ extern "C" int fdfb_blind_rotate(const fdfb_ctx* c, const void* brk, uint64_t* a
 
 static int keyswitch_rlwe(const fdfb_ctx* c, const u64* bpk, const u64* lwe, int count, u64* out, cudaStream_t st) {
   dim3 grd((2 * c->prm.N) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
+  TimedLaunch tl(c, FDFB_KCLASS_KEYSWITCH_RLWE, st);
   k_keyswitch_rlwe<<<grd, KS_COLS, 0, st>>>(c->dp, bpk, lwe, count, out);
   CKL(c);
   return FDFB_OK;
 }
 static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int count, u64* out, cudaStream_t st) {
   dim3 grd((c->prm.n + 1 + KS_COLS - 1) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
+  TimedLaunch tl(c, FDFB_KCLASS_KEYSWITCH_LWE, st);
   k_keyswitch_lwe<<<grd, KS_COLS, 0, st>>>(c->dp, ksk, lwe, count, out);
   CKL(c);
   return FDFB_OK;
@@ -663,6 +684,28 @@ extern "C" int fdfb_cdt_table(const fdfb_ctx* c, uint64_t* thr, int* T) {
   if (!c || !T) return FDFB_E_NULL;
   *T = c->dp.cdt_T;
   if (thr) for (size_t i = 0; i < c->cdt.size(); i++) thr[i] = c->cdt[i];
+  return FDFB_OK;
+}
+extern "C" int fdfb_timing_enable(const fdfb_ctx* c, int on) {
+  if (!c) return FDFB_E_NULL;
+  c->timing = on != 0;
+  return FDFB_OK;
+}
+extern "C" int fdfb_timing_read(const fdfb_ctx* c, int kclass, double* total_ms, uint64_t* launches) {
+  if (!c || !total_ms || !launches) return FDFB_E_NULL;
+  std::lock_guard<std::mutex> g(c->tmu);
+  double ms = 0; uint64_t cnt = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep;
+  for (auto& e : c->tev) {
+    if (e.first != kclass) { keep.push_back(e); continue; }
+    CK(cudaEventSynchronize(e.second.second));
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, e.second.first, e.second.second));
+    ms += f; cnt++;
+    cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second);
+  }
+  c->tev.swap(keep);
+  *total_ms = ms; *launches = cnt;
   return FDFB_OK;
 }
 extern "C" uint64_t fdfb_launch_count(const fdfb_ctx* c) { return c ? (uint64_t)c->launches.load() : 0; }

@@ -40,7 +40,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_lwe_encrypt", "fdfb_rlwe_encrypt", "fdfb_setup_lut", "fdfb_bootstrap_batch",
             "fdfb_bootstrap_batch_host", "fdfb_blind_rotate", "fdfb_sample_extract", "fdfb_lwe_keyswitch",
             "fdfb_vector_pack", "fdfb_shift", "fdfb_poly_mul", "fdfb_cdt_table", "fdfb_launch_count",
-            "fdfb_status_string", "fdfb_last_cuda_error"]
+            "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read"]
+KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3}
 
 
 def lib():
@@ -81,6 +82,8 @@ def lib():
         L.fdfb_status_string.argtypes = [C.c_int]
         L.fdfb_status_string.restype = C.c_char_p
         L.fdfb_last_cuda_error.restype = C.c_char_p
+        L.fdfb_timing_enable.argtypes = [vp, C.c_int]
+        L.fdfb_timing_read.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(u64)]
         _lib = L
     return _lib
 
@@ -155,6 +158,15 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().fdfb_launch_count(self.h))
+
+    def timing_enable(self, on: bool = True):
+        _check(lib().fdfb_timing_enable(self.h, 1 if on else 0))
+
+    def timing_read(self, kclass: str):
+        """(summed device ms, launches) of one kernel class since the last read."""
+        ms, cnt = C.c_double(), C.c_uint64()
+        _check(lib().fdfb_timing_read(self.h, KCLASS[kclass], C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
 
     # ---------------------------------------------------------------- keys
     def keygen(self, seed: int, which: int = 0x0F, sk=None, stream=None):
