@@ -78,7 +78,8 @@ enum { FDFB_KEY_BRK = 1, FDFB_KEY_BPK = 2, FDFB_KEY_KSK = 3, FDFB_KEY_PACK = 4,
 
 typedef struct fdfb_sizes_t {
   size_t sk_lwe, sk_rlwe;       /* bytes of the int8 secrets                        */
-  size_t brk, bpk, ksk, pack;   /* bytes of the OPAQUE device key formats            */
+  size_t brk, bpk, ksk, pack;   /* bytes of the OPAQUE device key formats (pack: canonical
+                                   table + suffix sums T1, Delta, U)      */
   size_t canon_brk, canon_bpk, canon_ksk, canon_pack;  /* canonical layouts (bytes) */
 } fdfb_sizes_t;
 
@@ -109,6 +110,10 @@ int fdfb_keygen_canonical(const fdfb_ctx* ctx, uint64_t seed, int kind, const in
                           void* stream);
 /* Convert a canonical key [dev] to the opaque device format [dev].  Syncs. */
 int fdfb_key_import(const fdfb_ctx* ctx, int kind, const uint64_t* canonical, void* dev_key, void* stream);
+
+/* Canonical layout of a device key [dev] -> canonical [dev] (BPK, KSK, PACK; BRK is
+ * held only in the NTT domain and returns FDFB_E_UNSUPPORTED).  Stream-ordered. */
+int fdfb_key_export(const fdfb_ctx* ctx, int kind, const void* dev_key, uint64_t* canonical, void* stream);
 
 /* ------------------------------------------------------------------ inputs
  * LWE encryptions of m[c] in Z_t (Delta = q_lwe/t) under sk_lwe,
@@ -142,17 +147,26 @@ int fdfb_bootstrap_batch_host(const fdfb_ctx* ctx, const void* brk, const void* 
 int fdfb_blind_rotate(const fdfb_ctx* ctx, const void* brk, uint64_t* acc, const uint32_t* abar,
                       uint32_t count, uint32_t acc_per_ct, void* stream);
 /* SampleExt (NSgn(0) = -1): rlwe [dev, B x 2N], k [dev, B, 1..N],
- * lwe [dev, B x (N+1)] mod Q. */
+ * lwe [dev, B x (N+1)] mod Q.  A k outside 1..N (device data, not checkable before
+ * launch) yields a zero row and raises the flag read by fdfb_device_status. */
 int fdfb_sample_extract(const fdfb_ctx* ctx, const uint64_t* rlwe, const uint32_t* k, uint64_t* lwe,
                         uint32_t B, void* stream);
 /* LWE KeySwitch N -> n mod q_lwe: in [dev, B x (N+1)] mod q_lwe. */
 int fdfb_lwe_keyswitch(const fdfb_ctx* ctx, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
                        uint32_t B, void* stream);
 /* VectorPack: lwe [dev, B x m x (N+1)] mod Q under s_F,
- * 1 <= m <= N; out [dev, B x 2N]. */
+ * 1 <= m <= N; out [dev, B x 2N] = sum_k Pack(lwe_k, pK, k), computed by the definition
+ * (m N ell key-row additions per item).  workspace may be NULL (size 0). */
 int fdfb_vector_pack(const fdfb_ctx* ctx, const void* pack, const uint64_t* lwe, uint32_t m, uint64_t* out,
                      uint32_t B, void* workspace, void* stream);
-/* Shift (readings F2/F3): rlwe_in [dev, B x 2N], d [dev, B, 1..N-1]. */
+/* Pack (reading G5): out[b] = [b X^{d-1}, 0] - X^{d-1} sum_{i,j}
+ * pK[i, j, A[i,j]+1] for lwe [dev, B x (N+1)] mod Q and d [dev, B, 1-based]. */
+int fdfb_pack(const fdfb_ctx* ctx, const void* pack, const uint64_t* lwe, const uint32_t* d, uint64_t* out,
+              uint32_t B, void* stream);
+/* Shift (readings F2/F3/G4): rlwe_in [dev, B x 2N] mod Q encrypting m,
+ * d [dev, B, 1..N-1] -> rlwe_out [dev, B x 2N] encrypting the cyclic rotation of m by d.
+ * Computed through the exact suffix-sum form of VectorPack.  A d outside
+ * 1..N-1 yields a zero row and raises the fdfb_device_status flag.  workspace may be NULL. */
 int fdfb_shift(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* d,
                uint64_t* rlwe_out, uint32_t B, void* workspace, void* stream);
 
@@ -171,6 +185,9 @@ enum { FDFB_KCLASS_BLIND_ROTATE = 0, FDFB_KCLASS_KEYSWITCH_RLWE = 1, FDFB_KCLASS
        FDFB_KCLASS_SHIFT = 3 };
 int fdfb_timing_enable(const fdfb_ctx* ctx, int on);
 int fdfb_timing_read(const fdfb_ctx* ctx, int kclass, double* total_ms, uint64_t* launches);
+/* Device-side argument errors of earlier stream-ordered calls: synchronises, returns
+ * FDFB_E_INDEX if any kernel saw an out-of-range k/d since the last clear, else FDFB_OK. */
+int fdfb_device_status(const fdfb_ctx* ctx, int clear);
 /* Number of kernel launches issued by this context so far (bench evidence). */
 uint64_t fdfb_launch_count(const fdfb_ctx* ctx);
 const char* fdfb_status_string(int status);

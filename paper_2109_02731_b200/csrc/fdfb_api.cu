@@ -23,6 +23,7 @@ struct fdfb_ctx {
   int num_sms;
   u64 qinv_neg, r2;          // Montgomery constants
   u64* d_tables;             // tw | twp | itw | itwp | cdt | omega tables
+  int* d_status;             // device-side argument errors (bit 0: index out of range)
   u64 omega_off;             // offset of NTT(X) slots (omega) in d_tables
   std::vector<u64> cdt;
   mutable std::atomic<unsigned long long> launches{0};
@@ -47,6 +48,11 @@ struct TimedLaunch {
 };
 
 static thread_local std::string g_last_cuda;
+struct PackLayout;
+static size_t shift_pack_bytes(const fdfb_params& p);
+static int pack_keygen(const fdfb_ctx* c, u64 seed, const int8_t* s_rlwe, void* pack, u64* shat, u64* tmask,
+                       u64* tprod, u64* tout, int CH, cudaStream_t st);
+static int pack_import(const fdfb_ctx* c, const u64* canon, void* dev, cudaStream_t st);
 
 #define CK(x)                                                              \
   do {                                                                     \
@@ -251,6 +257,8 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   c->omega_off = 4 * (size_t)N + c->cdt.size();
   for (int k = 0; k < N; k++) h[c->omega_off + k] = h_powmod(psi, 2 * (u64)bitrev(k, logN) + 1, Q);
   CK(cudaMalloc(&c->d_tables, ntab * sizeof(u64)));
+  CK(cudaMalloc(&c->d_status, sizeof(int)));
+  CK(cudaMemset(c->d_status, 0, sizeof(int)));
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));
@@ -282,6 +290,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
 extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   if (!c) return;
   cudaFree(c->d_tables);
+  cudaFree(c->d_status);
   delete c;
 }
 
@@ -486,6 +495,18 @@ extern "C" int fdfb_key_import(const fdfb_ctx* c, int kind, const uint64_t* cano
   return FDFB_OK;
 }
 
+extern "C" int fdfb_key_export(const fdfb_ctx* c, int kind, const void* dev_key, uint64_t* canon, void* stream) {
+  if (!c || !dev_key || !canon) return FDFB_E_NULL;
+  fdfb_sizes_t sz;
+  fdfb_sizes(c, &sz);
+  size_t bytes = kind == FDFB_KEY_BPK ? sz.canon_bpk : kind == FDFB_KEY_KSK ? sz.canon_ksk
+               : kind == FDFB_KEY_PACK ? sz.canon_pack : 0;
+  if (kind == FDFB_KEY_BRK) return FDFB_E_UNSUPPORTED;
+  if (!bytes) return FDFB_E_KIND;
+  CK(cudaMemcpyAsync(canon, dev_key, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  return FDFB_OK;
+}
+
 extern "C" int fdfb_lwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_lwe, const uint64_t* msg,
                                 uint32_t count, uint32_t flags, uint64_t* out, void* stream) {
   if (!c || !sk_lwe || !msg || !out) return FDFB_E_NULL;
@@ -646,7 +667,7 @@ extern "C" int fdfb_sample_extract(const fdfb_ctx* c, const uint64_t* rlwe, cons
   if (!c || !rlwe || !k || !lwe) return FDFB_E_NULL;
   if (!B) return FDFB_OK;
   size_t tot = (size_t)B * (c->prm.N + 1);
-  k_sample_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, S(stream)>>>(c->dp, rlwe, k, B, lwe);
+  k_sample_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, S(stream)>>>(c->dp, rlwe, k, B, lwe, c->d_status);
   CKL(c);
   return FDFB_OK;
 }
@@ -685,6 +706,13 @@ extern "C" int fdfb_cdt_table(const fdfb_ctx* c, uint64_t* thr, int* T) {
   *T = c->dp.cdt_T;
   if (thr) for (size_t i = 0; i < c->cdt.size(); i++) thr[i] = c->cdt[i];
   return FDFB_OK;
+}
+extern "C" int fdfb_device_status(const fdfb_ctx* c, int clear) {
+  if (!c) return FDFB_E_NULL;
+  int h = 0;
+  CK(cudaMemcpy(&h, c->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (clear) CK(cudaMemset(c->d_status, 0, sizeof(int)));
+  return (h & 1) ? FDFB_E_INDEX : FDFB_OK;
 }
 extern "C" int fdfb_timing_enable(const fdfb_ctx* c, int on) {
   if (!c) return FDFB_E_NULL;

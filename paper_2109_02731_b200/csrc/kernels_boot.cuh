@@ -328,13 +328,18 @@ __global__ void k_pubmux_finish(DevParams p, const u64* __restrict__ rotp, const
 
 // Standalone SampleExt with per-item 1-based k.
 __global__ void k_sample_extract(DevParams p, const u64* __restrict__ rlwe, const u32* __restrict__ kk, int B,
-                                 u64* __restrict__ lwe) {
+                                 u64* __restrict__ lwe, int* __restrict__ status) {
   const int N = p.N;
   size_t total = (size_t)B * (N + 1);
   for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
     size_t g = x / (N + 1); int I = (int)(x % (N + 1));
     const u64* ct = rlwe + g * 2 * N;
     int k = (int)kk[g];                      // 1-based
+    if (k < 1 || k > N) {                    // out of range: flag, zero output
+      if (I == 0) atomicOr(status, 1);
+      lwe[x] = 0;
+      continue;
+    }
     u64 v;
     if (I == 0) v = ct[k - 1];
     else {

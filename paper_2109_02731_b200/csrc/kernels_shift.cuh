@@ -1,9 +1,318 @@
 // kernels_shift.cuh -- Pack / VectorPack / Shift kernels.
+//
+// Device packing-key format (opaque; built by k_pack_suffix + k_pack_fixup from the
+// canonical PackSetup table pK[i][j][v], i in [N], j in [ell], v in [L]):
+//   A   canonical pK                     [N][ell][L][2][N]      (direct VectorPack / Pack)
+//   T1  T^{(v)}_{1,j}                    [ell][L][2][N]
+//   D   Delta^{(v)}_{i,j}, i = 2..N, v>=1 [ell][N-1][L-1][2][N]
+//   U   sum_j sum_{i>=2} T^{(0)}_{i,j}   [2][N]
+//   Uj  per-j partials of U              [ell][2][N]
+// with the key-only suffix sums  T^{(v)}_{i,j} = sum_{i'>=i} X^{i'-i} pK[i',j,v]  and
+// Delta^{(v)}_{i,j} = T^{(v)}_{i,j} - T^{(0)}_{i,j}.
+//
+// Shift: the m LWE samples Shift packs are
+// SampleExt(ct, K) at consecutive K = K1 .. K1+m-1, and SampleExt(ct, K).a[i+1] =
+// SampleExt(ct, K-1).a[i].  With A_k[i,j] = digit_j(a'_k[i]) this gives the exact identity
+//   sum_{k,i} X^{k-1} pK[i,j,A_k[i,j]] = sum_k X^{k-1} T^{(A_k[1,j])}_{1,j}
+//        + sum_{i'=1}^{N-1} ( T^{(gamma)}_{i'+1,j} - X^m T^{(beta)}_{i'+1,j} ),
+//   gamma = A_1[i'+1,j],  beta = A_m[i',j],
+// so VectorPack needs (m + 2(N-1)) * ell key-polynomial additions per ciphertext instead of
+// the definition's m * N * ell; the result is the same residue vector mod Q.
 #pragma once
 #include "kernels_core.cuh"
-struct fdfb_ctx;
-struct fdfb_params;
-static size_t shift_pack_bytes(const fdfb_params& p);
-static int pack_keygen(const fdfb_ctx* c, u64 seed, const int8_t* s_rlwe, void* pack, u64* shat, u64* tmask,
-                       u64* tprod, u64* tout, int CH, cudaStream_t st);
-static int pack_import(const fdfb_ctx* c, const u64* canon, void* dev, cudaStream_t st);
+
+struct PackLayout {
+  size_t P;                 // words per RLWE (2N)
+  size_t A, T1, D, U, Uj;   // word offsets
+  size_t words;
+};
+static inline PackLayout pack_layout(int N, int ell, int L) {
+  PackLayout l;
+  l.P = 2 * (size_t)N;
+  l.A = 0;
+  l.T1 = l.A + (size_t)N * ell * L * l.P;
+  l.D = l.T1 + (size_t)ell * L * l.P;
+  l.U = l.D + (size_t)ell * (N - 1) * (L - 1) * l.P;
+  l.Uj = l.U + l.P;
+  l.words = l.Uj + (size_t)ell * l.P;
+  return l;
+}
+
+// ---------------------------------------------------------------------------
+// Suffix recurrence T_i = P_i + X T_{i+1} (T_{N+1} = 0), one CTA per (j, v, column):
+//   v == 0: P_i = pK[i,j,0];          writes T1[j][0], accumulates Uj[j] = sum_{i>=2} T_i
+//   v >= 1: P_i = pK[i,j,v]-pK[i,j,0]; writes D[j][i][v] (i >= 2) and T1[j][v] (= Delta_1)
+// (X T)[c] = T[c-1] for c >= 1, -T[N-1] for c = 0.
+__global__ void k_pack_suffix(DevParams p, u64* __restrict__ pk, int ell, int L, PackLayout lay) {
+  extern __shared__ u64 sm[];
+  const int N = p.N;
+  const u64 Q = p.Q;
+  const int jv = blockIdx.x, col = blockIdx.y;
+  const int j = jv / L, v = jv % L;
+  u64* cur = sm;
+  u64* nxt = sm + N;
+  u64 uacc[8];                      // N <= 2048, blockDim 256 -> <= 8 coefficients per thread
+#pragma unroll
+  for (int r = 0; r < 8; r++) uacc[r] = 0;
+  for (int c = threadIdx.x; c < N; c += blockDim.x) cur[c] = 0;
+  __syncthreads();
+  for (int i = N; i >= 1; i--) {     // 1-based i
+    const u64* base = pk + lay.A + (((size_t)(i - 1) * ell + j) * L) * lay.P + (size_t)col * N;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const int c = threadIdx.x + r * blockDim.x;
+      if (c >= N) break;
+      u64 pi = base[(size_t)v * lay.P + c];
+      if (v) pi = sub_mod(pi, base[c], Q);
+      const u64 xt = c ? cur[c - 1] : neg_mod(cur[N - 1], Q);
+      const u64 t = add_mod(pi, xt, Q);
+      nxt[c] = t;
+      if (i >= 2) {
+        if (v) pk[lay.D + (((size_t)j * (N - 1) + (i - 2)) * (L - 1) + (v - 1)) * lay.P + (size_t)col * N + c] = t;
+        else uacc[r] = add_mod(uacc[r], t, Q);
+      } else {
+        pk[lay.T1 + ((size_t)j * L + v) * lay.P + (size_t)col * N + c] = t;
+      }
+    }
+    __syncthreads();
+    u64* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  if (v == 0) {
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const int c = threadIdx.x + r * blockDim.x;
+      if (c < N) pk[lay.Uj + (size_t)j * lay.P + (size_t)col * N + c] = uacc[r];
+    }
+  }
+}
+// T1[j][v] += T1[j][0] for v >= 1 (Delta_1 -> T_1), and U = sum_j Uj[j].
+__global__ void k_pack_fixup(DevParams p, u64* __restrict__ pk, int ell, int L, PackLayout lay) {
+  const u64 Q = p.Q;
+  const size_t P = lay.P;
+  const size_t n1 = (size_t)ell * (L - 1) * P;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n1 + P; x += (size_t)gridDim.x * blockDim.x) {
+    if (x < n1) {
+      const size_t w = x % P, jv = x / P;
+      const size_t j = jv / (L - 1), v = jv % (L - 1) + 1;
+      u64* t = pk + lay.T1 + (j * L + v) * P + w;
+      *t = add_mod(*t, pk[lay.T1 + (j * L) * P + w], Q);
+    } else {
+      const size_t w = x - n1;
+      u64 s = 0;
+      for (int j = 0; j < ell; j++) s = add_mod(s, pk[lay.Uj + (size_t)j * P + w], Q);
+      pk[lay.U + w] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SampleExt mask coefficient a'_K[i] (1-based K, i, NSgn(x) = +1 iff x > 0)
+FDFB_DEV u64 sx_mask(const u64* a, int K, int i, int N, u64 Q) {
+  const int idx = ((K - i) % N + N) % N;
+  const u64 v = a[idx];
+  return (K - i + 1 > 0) ? v : neg_mod(v, Q);
+}
+
+// Shift (readings F2/F3): one CTA per (tile of C ciphertexts, column h),
+// 256 threads, thread owns coefficients x_r = tid + 256 r (CPT = N / 256 of them).
+// BIN: L_pack == 2 (one Delta row per (i', j), shared by the whole tile).
+template <int CPT, int C, bool BIN>
+__global__ void __launch_bounds__(256)
+k_shift(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ ct,
+        const u32* __restrict__ dd, int B, u64* __restrict__ out, int* __restrict__ status) {
+  constexpr int TPB = 256;
+  const int N = p.N, h = blockIdx.y, tid = threadIdx.x;
+  const int ell = p.ell_pack, logL = p.logL_pack, L = 1 << logL;
+  const u64 Q = p.Q, dmask = (u64)L - 1;
+  extern __shared__ u64 sm[];
+  u64* gam = sm;                       // [C][N-1]: a'_{K1}[i'+1]
+  u64* bet = sm + (size_t)C * N;       // [C][N-1]: a'_{Km}[i']
+  u64* W = sm + (size_t)2 * C * N;     // [N] finalisation buffers
+  u64* Pb = W + N;
+  int m[C], K1[C], dv[C];
+  bool ok[C];
+#pragma unroll
+  for (int c = 0; c < C; c++) {
+    const int g = blockIdx.x * C + c;
+    ok[c] = g < B;
+    int d = ok[c] ? (int)dd[g] : 1;
+    if (d < 1 || d > N - 1) {          // out of range: flag, produce zeros for this item
+      if (ok[c] && tid == 0 && h == 0) atomicOr(status, 1);
+      ok[c] = false; d = 1;
+    }
+    dv[c] = d;
+    const bool br1 = 2 * d <= N;       // F3: d = N/2 takes branch 1
+    m[c] = br1 ? d : N - d;
+    K1[c] = br1 ? N - d + 1 : 1;
+    const u64* a = ct + (size_t)(ok[c] ? g : 0) * 2 * N + N;
+    const int Km = K1[c] + m[c] - 1;
+    for (int t = tid; t < N - 1; t += TPB) {
+      gam[(size_t)c * N + t] = ok[c] ? sx_mask(a, K1[c], t + 2, N, Q) : 0;
+      bet[(size_t)c * N + t] = ok[c] ? sx_mask(a, Km, t + 1, N, Q) : 0;
+    }
+  }
+  __syncthreads();
+  u64 G[C][CPT], Bs[C][CPT];
+#pragma unroll
+  for (int c = 0; c < C; c++)
+#pragma unroll
+    for (int r = 0; r < CPT; r++) { G[c][r] = 0; Bs[c][r] = 0; }
+
+  // sum_{i'} T^{(gamma)}_{i'+1,j} and sum_{i'} T^{(beta)}_{i'+1,j}, as Delta rows (T^{(0)} part is U)
+  for (int j = 0; j < ell; j++) {
+    const int sh = j * logL;
+    const u64* Dj = pk + lay.D + (size_t)j * (N - 1) * (L - 1) * lay.P + (size_t)h * N + tid;
+#pragma unroll 1
+    for (int t = 0; t < N - 1; t++) {
+      const u64* row = Dj + (size_t)t * (L - 1) * lay.P;
+      if (BIN) {
+        u64 rv[CPT];
+#pragma unroll
+        for (int r = 0; r < CPT; r++) rv[r] = __ldg(row + r * TPB);
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+          const u64 mg = 0 - ((gam[(size_t)c * N + t] >> sh) & 1);
+          const u64 mb = 0 - ((bet[(size_t)c * N + t] >> sh) & 1);
+#pragma unroll
+          for (int r = 0; r < CPT; r++) {
+            G[c][r] = csub(G[c][r] + (rv[r] & mg), Q);
+            Bs[c][r] = csub(Bs[c][r] + (rv[r] & mb), Q);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+          const u64 vg = (gam[(size_t)c * N + t] >> sh) & dmask;
+          const u64 vb = (bet[(size_t)c * N + t] >> sh) & dmask;
+          if (vg) {
+            const u64* rr = row + (vg - 1) * lay.P;
+#pragma unroll
+            for (int r = 0; r < CPT; r++) G[c][r] = csub(G[c][r] + __ldg(rr + r * TPB), Q);
+          }
+          if (vb) {
+            const u64* rr = row + (vb - 1) * lay.P;
+#pragma unroll
+            for (int r = 0; r < CPT; r++) Bs[c][r] = csub(Bs[c][r] + __ldg(rr + r * TPB), Q);
+          }
+        }
+      }
+    }
+  }
+  // sum_k X^{k-1} T^{(A_k[1,j])}_{1,j},  A_k[1,j] = digit_j(a[K_k - 1]),  K_k = K1 + k - 1
+  int mmax = 0;
+#pragma unroll
+  for (int c = 0; c < C; c++) mmax = (ok[c] && m[c] > mmax) ? m[c] : mmax;
+  for (int j = 0; j < ell; j++) {
+    const u64* T1j = pk + lay.T1 + (size_t)j * L * lay.P + (size_t)h * N;
+#pragma unroll 1
+    for (int k = 1; k <= mmax; k++) {
+#pragma unroll
+      for (int c = 0; c < C; c++) {
+        if (!ok[c] || k > m[c]) continue;
+        const int g = blockIdx.x * C + c;
+        const u64 av = __ldg(ct + (size_t)g * 2 * N + N + (K1[c] + k - 2));
+        const u64* T = T1j + ((av >> (j * logL)) & dmask) * lay.P;
+#pragma unroll
+        for (int r = 0; r < CPT; r++) {
+          const int e = tid + r * TPB - (k - 1);
+          const u64 tv = e >= 0 ? __ldg(T + e) : neg_mod(__ldg(T + e + N), Q);
+          G[c][r] = add_mod(G[c][r], tv, Q);
+        }
+      }
+    }
+  }
+  // finalisation per ciphertext:
+  //   S = G + U - X^m (U + Bs);  P = [sum_k b_k X^{k-1}, 0] - S  (column h)
+  //   branch 1: out = ct X^d + 2P;  branch 2: out = (2P - ct) X^d
+  const u64* U = pk + lay.U + (size_t)h * N;
+#pragma unroll
+  for (int c = 0; c < C; c++) {
+    if (!ok[c]) continue;                               // uniform across the CTA
+    const int g = blockIdx.x * C + c;
+    const u64* cth = ct + (size_t)g * 2 * N + (size_t)h * N;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) {
+      const int x = tid + r * TPB;
+      W[x] = add_mod(__ldg(U + x), Bs[c][r], Q);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) {
+      const int x = tid + r * TPB;
+      const int e = x - m[c];
+      const u64 rw = e >= 0 ? W[e] : neg_mod(W[e + N], Q);
+      const u64 S = sub_mod(add_mod(G[c][r], __ldg(U + x), Q), rw, Q);
+      u64 bs = 0;
+      if (h == 0 && x < m[c]) bs = __ldg(ct + (size_t)g * 2 * N + (K1[c] + x - 1));
+      Pb[x] = sub_mod(bs, S, Q);
+    }
+    __syncthreads();
+    const int d = dv[c];
+    const bool br1 = 2 * d <= N;
+    u64* o = out + (size_t)g * 2 * N + (size_t)h * N;
+#pragma unroll
+    for (int r = 0; r < CPT; r++) {
+      const int x = tid + r * TPB;
+      const u64 cr = rot_coeff(cth, x, d, N, Q);
+      if (br1) {
+        o[x] = add_mod(cr, add_mod(Pb[x], Pb[x], Q), Q);
+      } else {
+        const u64 pr = rot_coeff(Pb, x, d, N, Q);
+        o[x] = sub_mod(add_mod(pr, pr, Q), cr, Q);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// VectorPack by definition (Pack 1299-1306):
+//   out = sum_{k=1}^m X^{k-1+off} ([b_k, 0] - sum_{i,j} pK[i, j, A_k[i,j]]),  A_k = Decomp(a_k)
+// one CTA per (item, column); per k the key rows are summed unrotated (coalesced) into
+// smem, then rotated once.  off = 0 (VectorPack) or d-1 per item (Pack(c, pK, d)).
+template <int CPT>
+__global__ void __launch_bounds__(256)
+k_vector_pack(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ lwe, int m,
+              const u32* __restrict__ off, u64* __restrict__ out) {
+  constexpr int TPB = 256;
+  const int N = p.N, h = blockIdx.y, b = blockIdx.x, tid = threadIdx.x;
+  const int ell = p.ell_pack, logL = p.logL_pack, L = 1 << logL;
+  const u64 Q = p.Q, dmask = (u64)L - 1;
+  extern __shared__ u64 sm[];
+  u64* S = sm;                 // [N]
+  u64 acc[CPT];
+#pragma unroll
+  for (int r = 0; r < CPT; r++) acc[r] = 0;
+  const int o0 = off ? (int)off[b] : 0;
+  for (int k = 1; k <= m; k++) {
+    const u64* lw = lwe + ((size_t)b * m + (k - 1)) * (N + 1);
+    u64 s[CPT];
+#pragma unroll
+    for (int r = 0; r < CPT; r++) s[r] = 0;
+#pragma unroll 1
+    for (int i = 0; i < N; i++) {
+      const u64 ai = __ldg(lw + 1 + i);
+      for (int j = 0; j < ell; j++) {
+        const u64 v = (ai >> (j * logL)) & dmask;
+        const u64* row = pk + lay.A + (((size_t)i * ell + j) * L + v) * lay.P + (size_t)h * N + tid;
+#pragma unroll
+        for (int r = 0; r < CPT; r++) s[r] = add_mod(s[r], __ldg(row + r * TPB), Q);
+      }
+    }
+    // t = [b_k, 0] - s  (column h), then acc += X^{k-1+o0} t
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) {
+      const int x = tid + r * TPB;
+      u64 t = neg_mod(s[r], Q);
+      if (h == 0 && x == 0) t = add_mod(t, __ldg(lw), Q);
+      S[x] = t;
+    }
+    __syncthreads();
+    const int e = (k - 1 + o0) % (2 * N);
+#pragma unroll
+    for (int r = 0; r < CPT; r++) acc[r] = add_mod(acc[r], rot_coeff(S, tid + r * TPB, e, N, Q), Q);
+  }
+#pragma unroll
+  for (int r = 0; r < CPT; r++) out[(size_t)b * 2 * N + (size_t)h * N + tid + r * TPB] = acc[r];
+}

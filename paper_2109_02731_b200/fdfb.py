@@ -40,7 +40,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_lwe_encrypt", "fdfb_rlwe_encrypt", "fdfb_setup_lut", "fdfb_bootstrap_batch",
             "fdfb_bootstrap_batch_host", "fdfb_blind_rotate", "fdfb_sample_extract", "fdfb_lwe_keyswitch",
             "fdfb_vector_pack", "fdfb_shift", "fdfb_poly_mul", "fdfb_cdt_table", "fdfb_launch_count",
-            "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read"]
+            "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read",
+            "fdfb_pack", "fdfb_device_status", "fdfb_key_export"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3}
 
 
@@ -83,6 +84,9 @@ def lib():
         L.fdfb_status_string.restype = C.c_char_p
         L.fdfb_last_cuda_error.restype = C.c_char_p
         L.fdfb_timing_enable.argtypes = [vp, C.c_int]
+        L.fdfb_key_export.argtypes = [vp, C.c_int, vp, vp, vp]
+        L.fdfb_pack.argtypes = [vp, vp, vp, vp, vp, u32, vp]
+        L.fdfb_device_status.argtypes = [vp, C.c_int]
         L.fdfb_timing_read.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(u64)]
         _lib = L
     return _lib
@@ -198,6 +202,12 @@ class Context:
         _check(lib().fdfb_key_import(self.h, kind, _ptr(canonical.contiguous()), _ptr(dev), _stream(stream)))
         return dev
 
+    def key_export(self, kind: int, dev_key: torch.Tensor, stream=None):
+        name = {KEY_BPK: "canon_bpk", KEY_KSK: "canon_ksk", KEY_PACK: "canon_pack"}[kind]
+        out = self._u64(self.sizes[name] // 8)
+        _check(lib().fdfb_key_export(self.h, kind, _ptr(dev_key), _ptr(out), _stream(stream)))
+        return out
+
     # ---------------------------------------------------------------- inputs / LUT
     def lwe_encrypt(self, seed, s, msgs: torch.Tensor, exact=False, stream=None):
         out = self._u64(msgs.numel(), self.n + 1)
@@ -262,6 +272,16 @@ class Context:
         ws = self._bytes(lib().fdfb_workspace_vector_pack(self.h, m, B))
         _check(lib().fdfb_vector_pack(self.h, _ptr(pack), _ptr(lwe), m, _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
+
+    def pack(self, pack, lwe, d, stream=None):
+        B = lwe.shape[0]
+        out = self._u64(B, 2, self.N)
+        _check(lib().fdfb_pack(self.h, _ptr(pack), _ptr(lwe), _ptr(d), _ptr(out), B, _stream(stream)))
+        return out
+
+    def device_status(self, clear=True):
+        """Raise FdfbError if a kernel flagged an out-of-range k / d since the last clear."""
+        _check(lib().fdfb_device_status(self.h, 1 if clear else 0))
 
     def workspace_shift(self, B):
         return self._bytes(lib().fdfb_workspace_shift(self.h, B))

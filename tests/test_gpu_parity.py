@@ -197,3 +197,90 @@ def test_bootstrap_fhew_sampled():
     got = H(ctx.bootstrap_batch(dk, ctx.setup_lut(f), T(cts)))
     pick = [0, B - 1]
     assert np.array_equal(got[pick], orc.bootstrap(K, rotp, cts[pick]))
+
+
+# ----------------------------------------------------------------------------- Pack / VectorPack / Shift
+SHIFT512 = {  # mid-size Shift case on the BIN (L_pK = 2, ell = 54) path at 54-bit Q
+    "name": "shift512", "N": 512, "n": 64, "Q": 18014398509404161, "log_q_lwe": 52, "lwe_key": "ternary",
+    "rlwe_key": "ternary", "logL_rgsw": 14, "ell_rgsw": 4, "logL_boot": 8, "ell_boot": 7, "logL_pk": 14,
+    "ell_pk": 4, "logL_ks": 4, "ell_ks": 13, "logL_pack": 1, "ell_pack": 54, "t": 256, "sigma": 3.2,
+    "batch": 16, "seeds": {"keys": 9001, "msgs": 9002, "lut": 9003, "err": 9004}}
+
+_pcache = {}
+
+
+def pack_setup(name):
+    """Oracle PackSetup key (canonical) imported into the device format."""
+    if name not in _pcache:
+        cfg = SHIFT512 if name == "shift512" else synth.load_config(name)
+        orc = Oracle(cfg)
+        s, S = orc.keygen_secrets(cfg["seeds"]["keys"])
+        pk = orc.pack_key(cfg["seeds"]["keys"], S)
+        ctx = Context(cfg, 0)
+        dpk = ctx.key_import(KEY_PACK, T(pk.reshape(-1)))
+        _pcache[name] = (cfg, orc, s, S, pk, ctx, dpk)
+    return _pcache[name]
+
+
+def test_pack_key_device_format_from_keygen_equals_import():
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup("tiny_shift")
+    keys = ctx.keygen(cfg["seeds"]["keys"], which=0x11)
+    assert np.array_equal(H(keys["S"]), S)
+    assert torch.equal(keys["pack"], dpk)                       # canonical part and suffix sums
+    assert np.array_equal(H(ctx.key_export(KEY_PACK, dpk)), pk.reshape(-1))
+
+
+@pytest.mark.parametrize("name", ["tiny_shift", "shift512"])
+def test_vector_pack_and_pack(name):
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup(name)
+    N, Q = cfg["N"], cfg["Q"]
+    rng = np.random.default_rng(21)
+    for m in (1, 3, N if name == "tiny_shift" else 9):
+        v = rng.integers(0, Q, (2, m, N + 1), dtype=np.uint64)
+        got = H(ctx.vector_pack(dpk, T(v)))
+        for b in range(2):
+            assert np.array_equal(got[b], orc.vector_pack(pk, v[b])), (m, b)
+    c = rng.integers(0, Q, (4, N + 1), dtype=np.uint64)
+    d = np.array([1, 2, N // 2, N], dtype=np.uint32)
+    got = H(ctx.pack(dpk, T(c), T(d)))
+    for b in range(4):
+        assert np.array_equal(got[b], orc.pack(pk, c[b], int(d[b]))), b
+
+
+def test_shift_tiny_every_d_bit_exact():
+    """Every d in [1, N-1] (both branches, the d = N/2 tie) on the Tiny Shift config."""
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup("tiny_shift")
+    N = cfg["N"]
+    msg = synth.rlwe_messages(cfg, 1)
+    ct = orc.rlwe_encrypt(cfg["seeds"]["err"], S, msg)[0]
+    ds = np.arange(1, N, dtype=np.uint32)
+    cts = np.repeat(ct[None], len(ds), axis=0)
+    got = H(ctx.shift(dpk, T(cts), T(ds)))
+    ctx.device_status()
+    ref = orc.shift_batch(pk, cts, ds)
+    assert np.array_equal(got, ref)
+    for d in cfg["shift_d"]:                                    # the config's named cases decrypt to the rotation
+        assert np.array_equal((orc.rlwe_phase(S, got[d - 1]) - np.roll(msg[0], d).astype(np.int64)
+                               ).astype(np.int64).__abs__().max() < 2 ** 26, True)
+
+
+def test_shift_bin_path_bit_exact():
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup("shift512")
+    N = cfg["N"]
+    msg = synth.rlwe_messages(cfg, 13)
+    cts = orc.rlwe_encrypt(cfg["seeds"]["err"], S, msg)
+    ds = np.array([1, 2, 3, 100, 255, 256, 257, 300, 509, 510, 511, 17, 490], dtype=np.uint32)   # 13: ragged tile
+    got = H(ctx.shift(dpk, T(cts), T(ds)))
+    ctx.device_status()
+    assert np.array_equal(got, orc.shift_batch(pk, cts, ds))
+
+
+def test_shift_out_of_range_d_flagged():
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup("tiny_shift")
+    N = cfg["N"]
+    cts = np.zeros((3, 2, N), np.uint64)
+    got = H(ctx.shift(dpk, T(cts), T(np.array([0, 5, N], np.uint32))))
+    with pytest.raises(Exception):
+        ctx.device_status()
+    assert not got[0].any() and not got[2].any()
+    ctx.device_status()                                          # cleared
