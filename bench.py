@@ -25,12 +25,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# Integer-pipe peak: 148 SMs x 64 IMAD lanes/clk/SM
-# (fma pipe, 4 SMSPs x 16 lanes; measured by tools/intbench.cu) x 1965 MHz max SM clock.
+# Integer-multiply roofline: every IMAD-class
+# instruction issues on the fmaheavy pipe, 16 lanes/clk per SMSP = 64 lane-slots/clk/SM
+# (guide: fma pipe rt_SMSP = 2; tools/intbench.cu measures 64-70 IMAD lanes/SM/clk and
+# half that for IMAD.WIDE / IMAD.HI).  Peak = 148 SMs x 64 x 1965 MHz (max SM clock).
 IMAD_PER_SM_CLK = 64
-# Minimal IMAD-class instructions per lazy 64-bit Shoup modmul a*w - umulhi(a,w')*Q,
-# counted in the SASS of the NTT butterfly.
-IMAD_PER_MODMUL = 10
+# Slots per lazy 54-bit Shoup modmul a*w - umulhi(a,w')*Q as compiled for sm_100a:
+# 6 IMAD.WIDE (2 slots each) + 4 IMAD (1 slot) = 16 (SASS of tools/intbench.cu k_shoup64,
+# whose measured rate, 4 modmul/SM/clk at nominal clock, confirms it).
+IMAD_PER_MODMUL = 16
 
 
 def parse():
@@ -314,11 +317,12 @@ def main():
                     "h2d_bytes_per_step": B * (ctx.n + 1) * 8, "d2h_bytes_per_step": B * (ctx.n + 1) * 8,
                     "matches_device_path": e2e_ok},
             "roofline": {"kernel": "k_blind_rotate<2048>", "bound": "alu", "achieved": imad_s / 1e12,
-                         "peak": peak / 1e12, "unit": "TIMAD/s", "frac": imad_s / peak, "traffic": None,
+                         "peak": peak / 1e12, "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None,
                          "modmul_per_step": modmul_step, "imad_per_modmul": IMAD_PER_MODMUL,
                          "br_ms_per_step": br_ms / args.steps, "br_launches": br_launches,
                          "br_ms_per_launch": br_launch_ms, "br_share_of_step": (br_ms / args.steps) / ms_step,
-                         "peak_basis": "148 SM x 64 IMAD/clk x 1965 MHz (max clock)"},
+                         "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; 16 slots per 54-bit Shoup modmul",
+                         "modmul_per_s": modmul_step / (br_ms / args.steps / 1e3)},
             "clocks": clocks,
             "lut_spot_check": "%d/64 outputs decrypt to f(m)" % lut_ok,
             "keygen_s": keygen_s, "key_broadcast_s": bcast_s,

@@ -24,6 +24,8 @@ struct fdfb_ctx {
   u64 qinv_neg, r2;          // Montgomery constants
   u64* d_tables;             // tw | twp | itw | itwp | cdt | omega tables
   int* d_status;             // device-side argument errors (bit 0: index out of range)
+  u64x2* d_ftab;             // pass-grouped forward twiddle pairs (kernels_br.cuh)
+  u64x2* d_itab;             // pass-grouped inverse twiddle pairs
   u64 omega_off;             // offset of NTT(X) slots (omega) in d_tables
   std::vector<u64> cdt;
   mutable std::atomic<unsigned long long> launches{0};
@@ -171,7 +173,7 @@ template <int N>
 static int launch_br_t(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
                        cudaStream_t st) {
   constexpr int T = N / 8;
-  size_t sm = 4 * N * sizeof(u64);
+  size_t sm = 5 * N * sizeof(u64);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_blind_rotate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -183,7 +185,8 @@ static int launch_br_t(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, 
   int grid = c->num_sms * per_sm;
   if (grid > n_acc) grid = n_acc;
   TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
-  k_blind_rotate<N><<<grid, T, sm, st>>>(c->dp, bsk, accs, n_acc, acc_per_ct, abar);
+  k_blind_rotate<N><<<grid, T, sm, st>>>(c->dp, (const u64x2*)bsk, c->d_ftab, c->d_itab, accs, n_acc, acc_per_ct,
+                                         abar);
   CKL(c);
   return FDFB_OK;
 }
@@ -219,6 +222,34 @@ static int validate(const fdfb_params* p) {
   if ((u128)p->N * p->ell_pk * (1ULL << p->logL_pk) >= ((u128)1 << 32)) return FDFB_E_DECOMP;
   if (p->t < 2 || (2 * p->N) % p->t) return FDFB_E_PLAINTEXT;
   return FDFB_OK;
+}
+
+// Pass-grouped twiddle tables for kernels_br.cuh: for each radix-8 pass q and thread group
+// g the 7 pairs (tw[2^{3q}+g], tw[2^{3q+1}+2g+{0,1}], tw[2^{3q+2}+4g+{0..3}]); for the final
+// pass of P stages, per thread the pairs tw[2^{3 NMID+s} + tid 2^{3-P+s} + {0..2^{3-P+s}-1}].
+// tw(idx) = psi^{bitrev(idx)} (forward) or psi^{-bitrev(idx)} (inverse), with Shoup companions.
+template <int N>
+static void make_pass_tables(const std::vector<u64>& w, const std::vector<u64>& wp, std::vector<u64>& out) {
+  using S = BrShape<N>;
+  out.assign(2 * (size_t)S::PAIRS, 0);
+  auto put = [&](int pair, int idx) { out[2 * pair] = w[idx]; out[2 * pair + 1] = wp[idx]; };
+  for (int q = 0; q < S::NMID; q++) {
+    const int groups = 1 << (3 * q);
+    for (int g = 0; g < groups; g++) {
+      const int b = S::off(q) + 7 * g;
+      put(b, (1 << (3 * q)) + g);
+      for (int e = 0; e < 2; e++) put(b + 1 + e, (1 << (3 * q + 1)) + 2 * g + e);
+      for (int e = 0; e < 4; e++) put(b + 3 + e, (1 << (3 * q + 2)) + 4 * g + e);
+    }
+  }
+  for (int tid = 0; tid < S::T; tid++) {
+    int o = S::OFF_LAST + S::NLAST * tid;
+    for (int s = 0; s < S::PLAST; s++) {
+      const int cnt = 8 >> (S::PLAST - s);
+      for (int e = 0; e < cnt; e++) put(o + e, (1 << (3 * S::NMID + s)) + tid * cnt + e);
+      o += cnt;
+    }
+  }
 }
 
 extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out) {
@@ -258,6 +289,20 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   for (int k = 0; k < N; k++) h[c->omega_off + k] = h_powmod(psi, 2 * (u64)bitrev(k, logN) + 1, Q);
   CK(cudaMalloc(&c->d_tables, ntab * sizeof(u64)));
   CK(cudaMalloc(&c->d_status, sizeof(int)));
+  {
+    std::vector<u64> w(N), wp(N), wi(N), wip(N), ft, it;
+    for (int k = 0; k < N; k++) { w[k] = h[k]; wp[k] = h[N + k]; wi[k] = h[2 * N + k]; wip[k] = h[3 * N + k]; }
+    switch (N) {
+      case 256: make_pass_tables<256>(w, wp, ft); make_pass_tables<256>(wi, wip, it); break;
+      case 512: make_pass_tables<512>(w, wp, ft); make_pass_tables<512>(wi, wip, it); break;
+      case 1024: make_pass_tables<1024>(w, wp, ft); make_pass_tables<1024>(wi, wip, it); break;
+      default: make_pass_tables<2048>(w, wp, ft); make_pass_tables<2048>(wi, wip, it); break;
+    }
+    CK(cudaMalloc(&c->d_ftab, ft.size() * 8));
+    CK(cudaMalloc(&c->d_itab, it.size() * 8));
+    CK(cudaMemcpy(c->d_ftab, ft.data(), ft.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_itab, it.data(), it.size() * 8, cudaMemcpyHostToDevice));
+  }
   CK(cudaMemset(c->d_status, 0, sizeof(int)));
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
   DevParams& d = c->dp;
@@ -291,6 +336,8 @@ extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   if (!c) return;
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
+  cudaFree(c->d_ftab);
+  cudaFree(c->d_itab);
   delete c;
 }
 
@@ -377,7 +424,7 @@ static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, siz
   int rc = launch_ntt_batch(c, tmp, rows * 2, 0, st);
   if (rc) return rc;
   size_t tot = rows * 2 * N;
-  k_brk_finalize<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, tmp, dev + row0 * 2 * 2 * N, rows * 2);
+  k_brk_finalize<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, tmp, (u64x2*)dev + row0 * 2 * N, rows * 2);
   CKL(c);
   return FDFB_OK;
 }

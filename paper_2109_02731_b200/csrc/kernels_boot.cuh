@@ -1,6 +1,6 @@
 // kernels_boot.cuh -- the FDFB bootstrap hot path (Fig. Bootstrap).
 #pragma once
-#include "kernels_core.cuh"
+#include "kernels_br.cuh"
 
 // ---------------------------------------------------------------------------
 // a1: ModSwitch(ct, q_lwe, 2N) -- round half up.
@@ -36,110 +36,7 @@ __global__ void k_ladder_init(DevParams p, const u32* __restrict__ bbar, int B, 
   }
 }
 
-// ---------------------------------------------------------------------------
-// a3: batched blind rotation.  Persistent CTAs of N/8 threads;
-// each CTA keeps ONE accumulator resident in shared memory for all n*u CMux steps
-// and streams brK[i,j] (shared by every accumulator of the batch, L2-resident per
-// step) once per step.  One CMux step:
-//   d = acc X^e - acc (canonical), e = -abar_i u_j mod 2N
-//   for each of the 2*ell digit polynomials D_r = Decomp_{L,Q}(d)[r]:
-//       NTT(D_r) (registers + swizzled smem), MAC with brK[i,j][r] (Shoup, [0,2Q))
-//   acc += INTT(MAC) (N^{-1} folded into brK).
-template <int N>
-__global__ void __launch_bounds__(N / 8)
-k_blind_rotate(DevParams p, const u64* __restrict__ bsk, u64* __restrict__ accs, int n_acc, int acc_per_ct,
-               const u32* __restrict__ abar) {
-  constexpr int T = N / 8;
-  extern __shared__ u64 smem[];
-  u64* sacc = smem;            // [b | a], natural order, canonical
-  u64* sb0 = smem + 2 * N;     // NTT exchange buffers (double-buffered)
-  u64* sb1 = smem + 3 * N;
-  const int tid = threadIdx.x;
-  const u64 Q = p.Q, Q2 = p.Q2;
-  const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
-  const u64 dmask = (1ULL << logL) - 1;
-  const size_t step_stride = (size_t)2 * ell * 4 * N;
-
-  for (int g = blockIdx.x; g < n_acc; g += gridDim.x) {
-    u64* acc = accs + (size_t)g * 2 * N;
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
-    const u32* ab = abar + (size_t)(g / acc_per_ct) * p.n;
-    for (int i = 0; i < p.n; i++) {
-      const u32 ai = __ldg(ab + i);
-      for (int j = 0; j < u; j++) {
-        // exponent -abar_i * u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
-        const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
-        const u64* K = bsk + ((size_t)i * u + j) * step_stride;
-        __syncthreads();                                   // previous step's acc writes
-        u64 mb[8], ma[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
-        int buf = 0;
-#pragma unroll 1
-        for (int half = 0; half < 2; half++) {
-          const u64* src = sacc + half * N;
-          u64 d[8];
-#pragma unroll
-          for (int k = 0; k < 8; k++) {
-            const int pos = tid + T * k;
-            d[k] = sub_mod(rot_coeff(src, pos, e, N, Q), src[pos], Q);
-          }
-#pragma unroll 1
-          for (int r = 0; r < ell; r++) {
-            u64 x[8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) x[k] = (d[k] >> (r * logL)) & dmask;
-            ntt_fwd<N>(x, buf ? sb1 : sb0, tid, p);
-            buf ^= 1;
-            const u64* Kr = K + (size_t)(half * ell + r) * 4 * N + 8 * tid;
-            const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(Kr);
-            const ulonglong2* kbp = reinterpret_cast<const ulonglong2*>(Kr + N);
-            const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(Kr + 2 * N);
-            const ulonglong2* kap = reinterpret_cast<const ulonglong2*>(Kr + 3 * N);
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-              ulonglong2 w = __ldg(kb + v), wp = __ldg(kbp + v);
-              mb[2 * v] += mul_shoup_lazy(x[2 * v], w.x, wp.x, Q);
-              mb[2 * v + 1] += mul_shoup_lazy(x[2 * v + 1], w.y, wp.y, Q);
-            }
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-              ulonglong2 w = __ldg(ka + v), wp = __ldg(kap + v);
-              ma[2 * v] += mul_shoup_lazy(x[2 * v], w.x, wp.x, Q);
-              ma[2 * v + 1] += mul_shoup_lazy(x[2 * v + 1], w.y, wp.y, Q);
-            }
-          }
-        }
-        // sums of 2*ell terms in [0, 2Q): reduce into [0, 2Q) for the inverse transform
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          u64 vb = mb[k], va = ma[k];
-#pragma unroll
-          for (int s = 4; s >= 1; s--) { vb = csub(vb, Q << s); va = csub(va, Q << s); }
-          mb[k] = vb; ma[k] = va;
-        }
-        ntt_inv<N>(mb, buf ? sb1 : sb0, tid, p);
-        buf ^= 1;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const int pos = tid + T * k;
-          sacc[pos] = add_mod(sacc[pos], csub(mb[k], Q), Q);
-        }
-        ntt_inv<N>(ma, buf ? sb1 : sb0, tid, p);
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const int pos = N + tid + T * k;
-          sacc[pos] = add_mod(sacc[pos], csub(ma[k], Q), Q);
-        }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
-  }
-}
+// a3: batched blind rotation -> kernels_br.cuh
 
 // ---------------------------------------------------------------------------
 // a4: ladder SampleExt(acc, 1) + [L_boot^{i} 2^{-1}, 0]

@@ -221,19 +221,3 @@ __global__ void k_lwe_encrypt(DevParams p, u64 seed, const int8_t* s_lwe, const 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Device BRK format: [n*u][2ell rows][2 cols][val | shoup][N], NTT slots, values
-// pre-multiplied by N^{-1} (folded into the extProd's inverse transform).
-// in: canonical rows already forward-transformed (slots, [0,Q)) in `ntt_rows`.
-__global__ void k_brk_finalize(DevParams p, const u64* __restrict__ ntt_rows, u64* __restrict__ dev, size_t nrows) {
-  const int N = p.N;
-  size_t total = nrows * N;
-  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
-    size_t poly = x / N;  int c = (int)(x % N);
-    // poly = ((step*2ell + row)*2 + col)
-    u64 v = csub(mul_shoup_lazy(ntt_rows[x], p.ninv, p.ninvp, p.Q), p.Q);
-    u64 vp = (u64)(((unsigned __int128)v << 64) / p.Q);
-    dev[(poly * 2) * N + c] = v;
-    dev[(poly * 2 + 1) * N + c] = vp;
-  }
-}

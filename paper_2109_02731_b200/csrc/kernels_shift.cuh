@@ -283,7 +283,7 @@ k_vector_pack(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64
   u64 acc[CPT];
 #pragma unroll
   for (int r = 0; r < CPT; r++) acc[r] = 0;
-  const int o0 = off ? (int)off[b] : 0;
+  const int o0 = off ? (int)off[b] - 1 : 0;   // Pack(c, pK, d): message at X^{d-1}
   for (int k = 1; k <= m; k++) {
     const u64* lw = lwe + ((size_t)b * m + (k - 1)) * (N + 1);
     u64 s[CPT];
