@@ -24,8 +24,8 @@ struct fdfb_ctx {
   u64 qinv_neg, r2;          // Montgomery constants
   u64* d_tables;             // tw | twp | itw | itwp | cdt | omega tables
   int* d_status;             // device-side argument errors (bit 0: index out of range)
-  u64x2* d_ftab;             // pass-grouped forward twiddle pairs (kernels_br.cuh)
-  u64x2* d_itab;             // pass-grouped inverse twiddle pairs
+  RnsParams rns;             // word-size primes for the exact RNS external product (kernels_br.cuh)
+  u32* d_rtab;               // [2 dirs][np][GROUPS][8 pairs] twiddle tables
   u64 omega_off;             // offset of NTT(X) slots (omega) in d_tables
   std::vector<u64> cdt;
   mutable std::atomic<unsigned long long> launches{0};
@@ -169,35 +169,40 @@ static int launch_ntt_batch(const fdfb_ctx* c, u64* data, size_t count, int mode
   return FDFB_OK;
 }
 
-template <int N>
-static int launch_br_t(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
+template <int N, int NP>
+static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
                        cudaStream_t st) {
   constexpr int T = N / 8;
-  size_t sm = 5 * N * sizeof(u64);
+  const size_t sm = 56 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange 8N + Garner staging 16N bytes
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_blind_rotate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_blind_rotate<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr_set = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate<N>, T, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate<N, NP>, T, sm);
   if (per_sm < 1) per_sm = 1;
   int grid = c->num_sms * per_sm;
   if (grid > n_acc) grid = n_acc;
   TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
-  k_blind_rotate<N><<<grid, T, sm, st>>>(c->dp, (const u64x2*)bsk, c->d_ftab, c->d_itab, accs, n_acc, acc_per_ct,
-                                         abar);
+  k_blind_rotate<N, NP><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar);
   CKL(c);
   return FDFB_OK;
 }
 static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
                      cudaStream_t st) {
   if (n_acc <= 0) return FDFB_OK;
+  const u32* k = (const u32*)bsk;
+  const bool three = c->rns.np == 3;
   switch (c->prm.N) {
-    case 256: return launch_br_t<256>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
-    case 512: return launch_br_t<512>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
-    case 1024: return launch_br_t<1024>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
-    case 2048: return launch_br_t<2048>(c, bsk, accs, n_acc, acc_per_ct, abar, st);
+    case 256: return three ? launch_br_t<256, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
+                           : launch_br_t<256, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
+    case 512: return three ? launch_br_t<512, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
+                           : launch_br_t<512, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
+    case 1024: return three ? launch_br_t<1024, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
+                            : launch_br_t<1024, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
+    case 2048: return three ? launch_br_t<2048, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
+                            : launch_br_t<2048, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
   }
   return FDFB_E_DIMENSION;
 }
@@ -224,32 +229,105 @@ static int validate(const fdfb_params* p) {
   return FDFB_OK;
 }
 
-// Pass-grouped twiddle tables for kernels_br.cuh: for each radix-8 pass q and thread group
-// g the 7 pairs (tw[2^{3q}+g], tw[2^{3q+1}+2g+{0,1}], tw[2^{3q+2}+4g+{0..3}]); for the final
-// pass of P stages, per thread the pairs tw[2^{3 NMID+s} + tid 2^{3-P+s} + {0..2^{3-P+s}-1}].
-// tw(idx) = psi^{bitrev(idx)} (forward) or psi^{-bitrev(idx)} (inverse), with Shoup companions.
+// Pass-grouped RNS twiddle tables for kernels_br.cuh (one prime, one direction): group g of
+// radix-8 pass q holds (tw[2^{3q}+g], tw[2^{3q+1}+2g+{0,1}], tw[2^{3q+2}+4g+{0..3}], pad);
+// the final pass of P stages has one group per thread with, for stage s, the pairs
+// tw[2^{3 NMID+s} + tid c_s + {0..c_s-1}], c_s = 8 >> (P-s).  tw(idx) = psi^{+-bitrev(idx)}
+// mod p with its 32-bit Shoup companion.  Appends GROUPS*16 words to out.
 template <int N>
-static void make_pass_tables(const std::vector<u64>& w, const std::vector<u64>& wp, std::vector<u64>& out) {
+static void make_rns_tables(u64 psi, u64 pr, std::vector<u32>& out) {
   using S = BrShape<N>;
-  out.assign(2 * (size_t)S::PAIRS, 0);
-  auto put = [&](int pair, int idx) { out[2 * pair] = w[idx]; out[2 * pair + 1] = wp[idx]; };
+  const int logN = S::LOGN;
+  std::vector<u32> w(N), ws(N);
+  for (int k = 0; k < N; k++) {
+    w[k] = (u32)h_powmod(psi, bitrev(k, logN), pr);
+    ws[k] = (u32)(((u64)w[k] << 32) / pr);
+  }
+  const size_t base = out.size();
+  out.resize(base + (size_t)S::GROUPS * 16, 0);
+  auto put = [&](int grp, int e, int idx) {
+    out[base + (size_t)grp * 16 + 2 * e] = w[idx];
+    out[base + (size_t)grp * 16 + 2 * e + 1] = ws[idx];
+  };
   for (int q = 0; q < S::NMID; q++) {
     const int groups = 1 << (3 * q);
     for (int g = 0; g < groups; g++) {
-      const int b = S::off(q) + 7 * g;
-      put(b, (1 << (3 * q)) + g);
-      for (int e = 0; e < 2; e++) put(b + 1 + e, (1 << (3 * q + 1)) + 2 * g + e);
-      for (int e = 0; e < 4; e++) put(b + 3 + e, (1 << (3 * q + 2)) + 4 * g + e);
+      const int G = S::grp(q) + g;
+      put(G, 0, (1 << (3 * q)) + g);
+      for (int e = 0; e < 2; e++) put(G, 1 + e, (1 << (3 * q + 1)) + 2 * g + e);
+      for (int e = 0; e < 4; e++) put(G, 3 + e, (1 << (3 * q + 2)) + 4 * g + e);
     }
   }
   for (int tid = 0; tid < S::T; tid++) {
-    int o = S::OFF_LAST + S::NLAST * tid;
+    int o = 0;
     for (int s = 0; s < S::PLAST; s++) {
       const int cnt = 8 >> (S::PLAST - s);
-      for (int e = 0; e < cnt; e++) put(o + e, (1 << (3 * S::NMID + s)) + tid * cnt + e);
+      for (int e = 0; e < cnt; e++) put(S::G_LAST + tid, o + e, (1 << (3 * S::NMID + s)) + tid * cnt + e);
       o += cnt;
     }
   }
+}
+static u64 h_inv(u64 a, u64 m) { return h_powmod(a % m, m - 2, m); }   // m prime
+static u64 h_primroot_2n(u64 pr, int N) {
+  for (u64 g = 2; g < 10000; g++) {
+    u64 c = h_powmod(g, (pr - 1) / (2 * (u64)N), pr);
+    if (h_powmod(c, N, pr) == pr - 1) return c;
+  }
+  return 0;
+}
+// Choose the RNS primes (largest p < 2^30, p = 1 mod 2N) so that prod p > 2 * bound + 1 with
+// bound = 2 ell N (L-1) (Q-1) >= |coefficients| of sum_r D_r * K_r; build constants/tables.
+static int setup_rns(fdfb_ctx* c) {
+  const fdfb_params& p = c->prm;
+  const int N = p.N;
+  RnsParams& R = c->rns;
+  memset(&R, 0, sizeof(R));
+  const u128 bound = (u128)(2 * p.ell_rgsw) * N * ((1ULL << p.logL_rgsw) - 1) * (p.Q - 1);
+  std::vector<u64> primes;
+  u128 P = 1;
+  for (u64 cand = ((1ULL << 30) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 29) && primes.size() < RNS_MAXP;
+       cand -= 2 * (u64)N) {
+    if (cand >= (1ULL << 30) || cand == p.Q || !h_is_prime(cand)) continue;
+    primes.push_back(cand);
+    P *= cand;
+    if (primes.size() >= 2 && P / 2 > bound + 1) break;
+  }
+  if (primes.size() < 2 || P / 2 <= bound + 1) return FDFB_E_UNSUPPORTED;
+  R.np = (int)primes.size();
+  const u64 Q = p.Q;
+  std::vector<u32> ft, it;
+  for (int i = 0; i < R.np; i++) {
+    const u64 pr = primes[i];
+    R.p[i] = (u32)pr; R.p2[i] = (u32)(2 * pr);
+    R.r32[i] = (u32)((1ULL << 32) % pr); R.r32s[i] = (u32)(((u64)R.r32[i] << 32) / pr);
+    R.b32[i] = (u32)((1ULL << 32) / pr);
+    R.ninv[i] = (u32)h_inv(N, pr); R.ninvs[i] = (u32)(((u64)R.ninv[i] << 32) / pr);
+    const u64 psi = h_primroot_2n(pr, N);
+    if (!psi) return FDFB_E_UNSUPPORTED;
+    const u64 psii = h_inv(psi, pr);
+    switch (N) {
+      case 256: make_rns_tables<256>(psi, pr, ft); make_rns_tables<256>(psii, pr, it); break;
+      case 512: make_rns_tables<512>(psi, pr, ft); make_rns_tables<512>(psii, pr, it); break;
+      case 1024: make_rns_tables<1024>(psi, pr, ft); make_rns_tables<1024>(psii, pr, it); break;
+      default: make_rns_tables<2048>(psi, pr, ft); make_rns_tables<2048>(psii, pr, it); break;
+    }
+  }
+  auto s32 = [](u64 w, u64 m) { return (u32)((w << 32) / m); };
+  R.g01 = (u32)h_inv(primes[0], primes[1]); R.g01s = s32(R.g01, primes[1]);
+  if (R.np == 3) {
+    R.g02 = (u32)h_inv(h_mulmod(primes[0], primes[1], primes[2]), primes[2]); R.g02s = s32(R.g02, primes[2]);
+    R.g12 = (u32)h_inv(primes[1], primes[2]); R.g12s = s32(R.g12, primes[2]);
+  }
+  R.m0 = 1 % Q; R.m0s = shoup_of(R.m0, Q);
+  R.m1 = primes[0] % Q; R.m1s = shoup_of(R.m1, Q);
+  R.m2 = R.np == 3 ? h_mulmod(primes[0] % Q, primes[1] % Q, Q) : 0; R.m2s = shoup_of(R.m2, Q);
+  R.pmq = (u64)(P % Q);
+  ft.insert(ft.end(), it.begin(), it.end());
+  CK(cudaMalloc(&c->d_rtab, ft.size() * 4));
+  CK(cudaMemcpy(c->d_rtab, ft.data(), ft.size() * 4, cudaMemcpyHostToDevice));
+  R.ftab = (const uint4*)c->d_rtab;
+  R.itab = (const uint4*)(c->d_rtab + it.size());
+  return FDFB_OK;
 }
 
 extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out) {
@@ -289,22 +367,9 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   for (int k = 0; k < N; k++) h[c->omega_off + k] = h_powmod(psi, 2 * (u64)bitrev(k, logN) + 1, Q);
   CK(cudaMalloc(&c->d_tables, ntab * sizeof(u64)));
   CK(cudaMalloc(&c->d_status, sizeof(int)));
-  {
-    std::vector<u64> w(N), wp(N), wi(N), wip(N), ft, it;
-    for (int k = 0; k < N; k++) { w[k] = h[k]; wp[k] = h[N + k]; wi[k] = h[2 * N + k]; wip[k] = h[3 * N + k]; }
-    switch (N) {
-      case 256: make_pass_tables<256>(w, wp, ft); make_pass_tables<256>(wi, wip, it); break;
-      case 512: make_pass_tables<512>(w, wp, ft); make_pass_tables<512>(wi, wip, it); break;
-      case 1024: make_pass_tables<1024>(w, wp, ft); make_pass_tables<1024>(wi, wip, it); break;
-      default: make_pass_tables<2048>(w, wp, ft); make_pass_tables<2048>(wi, wip, it); break;
-    }
-    CK(cudaMalloc(&c->d_ftab, ft.size() * 8));
-    CK(cudaMalloc(&c->d_itab, it.size() * 8));
-    CK(cudaMemcpy(c->d_ftab, ft.data(), ft.size() * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->d_itab, it.data(), it.size() * 8, cudaMemcpyHostToDevice));
-  }
   CK(cudaMemset(c->d_status, 0, sizeof(int)));
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
+  if ((rc = setup_rns(c))) { delete c; return rc; }
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));
   d.Q = Q; d.Q2 = 2 * Q; d.Q4 = 4 * Q; d.half = (Q + 1) / 2;
@@ -336,8 +401,7 @@ extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   if (!c) return;
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
-  cudaFree(c->d_ftab);
-  cudaFree(c->d_itab);
+  cudaFree(c->d_rtab);
   delete c;
 }
 
@@ -348,7 +412,7 @@ extern "C" int fdfb_sizes(const fdfb_ctx* c, fdfb_sizes_t* o) {
   const fdfb_params& p = c->prm;
   o->sk_lwe = p.n; o->sk_rlwe = p.N;
   o->canon_brk = brk_words(p) * 8;
-  o->brk = o->canon_brk * 2;
+  o->brk = brk_words(p) * c->rns.np * 4;        // u32 residues per RNS prime
   o->canon_bpk = (size_t)p.N * p.ell_pk * 2 * p.N * 8;
   o->bpk = o->canon_bpk;
   o->canon_ksk = (size_t)p.N * p.ell_ks * (p.n + 1) * 8;
@@ -415,18 +479,24 @@ static int make_shat(const fdfb_ctx* c, const int8_t* s_rlwe, u64* shat, cudaStr
   return launch_ntt_batch(c, shat, 1, 0, st);
 }
 
-// canonical brk rows [rows][2][N] (coef) -> device BRK; rows are consecutive canonical rows
-// starting at row0 (flat (i*u+j)*2ell + row).  tmp: rows*2*N words.
-static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, size_t row0, u64* dev, u64* tmp,
-                           cudaStream_t st) {
-  const int N = c->prm.N;
-  CK(cudaMemcpyAsync(tmp, canon, rows * 2 * N * 8, cudaMemcpyDeviceToDevice, st));
-  int rc = launch_ntt_batch(c, tmp, rows * 2, 0, st);
-  if (rc) return rc;
-  size_t tot = rows * 2 * N;
-  k_brk_finalize<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, tmp, (u64x2*)dev + row0 * 2 * N, rows * 2);
+// canonical brk rows [rows][2][N] (coef) -> device BRK (RNS NTT domain); rows are consecutive
+// canonical rows starting at row0 (flat (i*u+j)*2ell + row).
+template <int N>
+static int brk_rns_t(const fdfb_ctx* c, const u64* canon, size_t rows, size_t row0, u32* dev, cudaStream_t st) {
+  dim3 g((unsigned)(rows * 2), c->rns.np);
+  k_brk_rns<N><<<g, N / 8, 0, st>>>(c->dp, c->rns, canon, row0, dev);
   CKL(c);
   return FDFB_OK;
+}
+static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, size_t row0, u64* dev, u64* /*tmp*/,
+                           cudaStream_t st) {
+  switch (c->prm.N) {
+    case 256: return brk_rns_t<256>(c, canon, rows, row0, (u32*)dev, st);
+    case 512: return brk_rns_t<512>(c, canon, rows, row0, (u32*)dev, st);
+    case 1024: return brk_rns_t<1024>(c, canon, rows, row0, (u32*)dev, st);
+    case 2048: return brk_rns_t<2048>(c, canon, rows, row0, (u32*)dev, st);
+  }
+  return FDFB_E_DIMENSION;
 }
 
 extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int8_t* sk_lwe, int8_t* sk_rlwe,

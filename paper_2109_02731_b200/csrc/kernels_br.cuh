@@ -1,23 +1,31 @@
 // kernels_br.cuh -- the batched blind rotation, the hot kernel.
 //
-// One CTA of T = N/8 threads per accumulator, resident in shared memory for all n*u CMux
-// steps; 512/T CTAs per SM (<= 128 registers per thread) so that two (N = 2048) or more
-// accumulators interleave on every SM and hide each other's latencies and barriers.
-// One CMux step (CMux = extProd(brK[i,j], acc X^e - acc) + acc):
-//   d = acc X^e - acc (canonical, thread-private scratch in smem)
-//   for each of the 2 ell digit polynomials D_r = Decomp_{L,Q}(d)[r]:
-//       forward NTT of D_r in registers (radix-8 passes, one smem exchange per pass),
-//       Shoup MAC with brK[i,j][r] for both output columns (lazy, [0, 16Q))
-//   acc += INTT(MAC) for both columns (N^{-1} folded into brK).
+// One CTA of T = N/8 threads per accumulator; the accumulator (canonical, mod Q) stays in
+// shared memory for all n*u CMux steps; 512/T CTAs per SM (<= 128 registers per thread).
+// One CMux step (CMux(C, g, h) = extProd(C, g - h) + h; extProd 2906):
+//   d = acc X^e - acc,  D_r = Decomp_{L,Q}(d)[r] (unsigned digits < L)
+//   acc_c += ( sum_{r < 2 ell} D_r * brK[i,j][r][c] ) mod Q          for c in {b, a}
 //
-// Twiddles come from pass-grouped tables of (w, w') pairs (built on the host, see
-// fdfb_api.cu make_pass_tables): for every radix-8 pass a thread needs only the 7 (or
-// 8 - 8/2^PLAST) pairs of its group, stored contiguously -> one base address per pass and
-// 16-byte loads with immediate offsets (no per-butterfly 64-bit address arithmetic).
-// brK device format: [n*u steps][2 ell rows][2 cols][N slots] of (w, w') pairs, NTT
-// (bit-reversed) slot order, w pre-multiplied by N^{-1}.
+// Exact RNS evaluation of the external product.  The products D_r * K (negacyclic, over
+// the integers, K in [0, Q)) have |coefficients| < 2 ell N (L-1) Q (< 2^82 at the Large
+// configuration), so they are computed exactly modulo NP word-size NTT primes p_i < 2^30
+// (P = prod p_i > 2 * bound) with 32-bit Harvey/Shoup arithmetic, and the signed integer
+// result is recovered by Garner CRT and reduced mod Q.  The result is the same residue
+// vector as the schoolbook definition (bit-exact with any correct evaluation); it costs
+// ~4 IMAD slots per 30-bit butterfly instead of ~16-22 for a 54-bit Shoup butterfly.
+//
+// Per CMux and prime p: 2 ell forward NTT_p of the digit polynomials (registers, radix-8
+// passes, one smem exchange each, u32), lazy 64-bit MAC against the NTT_p-domain key
+// (u32, N^{-1} folded in), one reduction, 2 inverse NTT_p; after the last prime, Garner
+// CRT per coefficient and acc += V mod Q.
+//
+// Twiddles: pass-grouped tables of (w, w') u32 pairs per prime (fdfb_api.cu
+// make_rns_tables), 8 pairs per group (7 used) -> one base per pass, 16-byte loads.
+// brK device format: [n*u steps][NP primes][2 ell rows][2 cols][N slots] u32.
 #pragma once
 #include "kernels_core.cuh"
+
+#define RNS_MAXP 3
 
 template <int N>
 struct BrShape {
@@ -27,89 +35,121 @@ struct BrShape {
   static constexpr int PLAST = LOGN - 3 * NMID;    // stages of the final pass (1..3)
   static constexpr int NLAST = 8 - (8 >> PLAST);   // twiddle pairs per thread in the final pass
   static constexpr int MINB = 512 / T;             // CTAs per SM
-  // offsets (in pairs) of each pass's table
-  static constexpr int off(int q) {                // q in [0, NMID): 7 * sum_{q'<q} 8^{q'}
+  static constexpr int grp(int q) {                // groups before pass q (8 pairs per group)
     int o = 0, g = 1;
-    for (int i = 0; i < q; i++) { o += 7 * g; g *= 8; }
+    for (int i = 0; i < q; i++) { o += g; g *= 8; }
     return o;
   }
-  static constexpr int OFF_LAST = off(NMID);
-  static constexpr int PAIRS = OFF_LAST + T * NLAST;
+  static constexpr int G_LAST = grp(NMID);
+  static constexpr int GROUPS = G_LAST + T;        // one group per thread in the final pass
+  static constexpr int PAIRS = 8 * GROUPS;         // per prime and direction
 };
 
-typedef ulonglong2 u64x2;
+// Per-context RNS constants (passed by value).
+struct RnsParams {
+  int np;
+  u32 p[RNS_MAXP], p2[RNS_MAXP];          // primes, 2p
+  u32 r32[RNS_MAXP], r32s[RNS_MAXP];      // 2^32 mod p and its Shoup companion
+  u32 b32[RNS_MAXP];                      // floor(2^32 / p)  (reduction of a 32-bit word)
+  u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} mod p (key import)
+  // Garner: c1 = (r1 - c0) g01 mod p1;  c2 = (r2 - c0) g02 - c1 g12 mod p2
+  u32 g01, g01s, g02, g02s, g12, g12s;
+  u64 m0, m0s, m1, m1s, m2, m2s;          // 1, p0, p0 p1 mod Q (+ 64-bit Shoup companions)
+  u64 pmq;                                // P mod Q (sign correction)
+  const uint4* ftab;                      // [np][GROUPS][8 pairs] forward (w, w') u32
+  const uint4* itab;                      // inverse
+};
 
-FDFB_DEV u64x2 ldp(const u64x2* p) { return __ldg(p); }
+FDFB_DEV u32 shoup32(u32 a, u32 w, u32 ws, u32 p) {     // a*w mod p in [0, 2p), any a < 2^32
+  const u32 q = __umulhi(a, ws);
+  return a * w - q * p;
+}
+FDFB_DEV u32 csub32(u32 x, u32 m) { return min(x, x - m); }
 
-FDFB_DEV void bfw(u64& X, u64& Y, u64x2 w, u64 Q, u64 Q2) {      // Harvey CT, in/out [0, 4Q)
-  u64 x = csub(X, Q2);
-  u64 t = mul_shoup_lazy(Y, w.x, w.y, Q);
+FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // Harvey CT, [0, 4p)
+  const u32 x = csub32(X, p2);
+  const u32 t = shoup32(Y, w, ws, p);
   X = x + t;
-  Y = x - t + Q2;
+  Y = x - t + p2;
 }
-FDFB_DEV void bin(u64& X, u64& Y, u64x2 w, u64 Q, u64 Q2) {      // Harvey GS, in/out [0, 2Q)
-  u64 x = X, y = Y;
-  X = csub(x + y, Q2);
-  Y = mul_shoup_lazy(x - y + Q2, w.x, w.y, Q);
+FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // Harvey GS, [0, 2p)
+  const u32 x = X, y = Y;
+  X = csub32(x + y, p2);
+  Y = shoup32(x - y + p2, w, ws, p);
 }
 
-// forward radix-8 pass: 3 stages on x[0..7] (pair distances 4, 2, 1 in k); tw -> the group's 7 pairs
-FDFB_DEV void fwd8(u64 x[8], const u64x2* tw, u64 Q, u64 Q2) {
-  const u64x2 w0 = ldp(tw);
+// 8 pairs of a group: tw[0] stage-0, tw[1..2] stage-1, tw[3..6] stage-2 (tw[7] padding)
+struct Tw8 { u32 w[8], s[8]; };
+FDFB_DEV void load_tw8(Tw8& t, const uint4* g) {
 #pragma unroll
-  for (int k = 0; k < 4; k++) bfw(x[k], x[k + 4], w0, Q, Q2);
-  const u64x2 w1 = ldp(tw + 1), w2 = ldp(tw + 2);
-  bfw(x[0], x[2], w1, Q, Q2); bfw(x[1], x[3], w1, Q, Q2);
-  bfw(x[4], x[6], w2, Q, Q2); bfw(x[5], x[7], w2, Q, Q2);
-#pragma unroll
-  for (int k = 0; k < 4; k++) bfw(x[2 * k], x[2 * k + 1], ldp(tw + 3 + k), Q, Q2);
+  for (int i = 0; i < 4; i++) {
+    const uint4 v = __ldg(g + i);
+    t.w[2 * i] = v.x; t.s[2 * i] = v.y; t.w[2 * i + 1] = v.z; t.s[2 * i + 1] = v.w;
+  }
 }
-FDFB_DEV void inv8(u64 x[8], const u64x2* tw, u64 Q, u64 Q2) {
+FDFB_DEV void fwd8_32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+  Tw8 t; load_tw8(t, g);
 #pragma unroll
-  for (int k = 0; k < 4; k++) bin(x[2 * k], x[2 * k + 1], ldp(tw + 3 + k), Q, Q2);
-  const u64x2 w1 = ldp(tw + 1), w2 = ldp(tw + 2);
-  bin(x[0], x[2], w1, Q, Q2); bin(x[1], x[3], w1, Q, Q2);
-  bin(x[4], x[6], w2, Q, Q2); bin(x[5], x[7], w2, Q, Q2);
-  const u64x2 w0 = ldp(tw);
+  for (int k = 0; k < 4; k++) bfw32(x[k], x[k + 4], t.w[0], t.s[0], p, p2);
+  bfw32(x[0], x[2], t.w[1], t.s[1], p, p2); bfw32(x[1], x[3], t.w[1], t.s[1], p, p2);
+  bfw32(x[4], x[6], t.w[2], t.s[2], p, p2); bfw32(x[5], x[7], t.w[2], t.s[2], p, p2);
 #pragma unroll
-  for (int k = 0; k < 4; k++) bin(x[k], x[k + 4], w0, Q, Q2);
+  for (int k = 0; k < 4; k++) bfw32(x[2 * k], x[2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
 }
-// final pass on positions 8 tid + k: P stages with pair distance t = 2^{P-1-s}
+FDFB_DEV void inv8_32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+  Tw8 t; load_tw8(t, g);
+#pragma unroll
+  for (int k = 0; k < 4; k++) bin32(x[2 * k], x[2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
+  bin32(x[0], x[2], t.w[1], t.s[1], p, p2); bin32(x[1], x[3], t.w[1], t.s[1], p, p2);
+  bin32(x[4], x[6], t.w[2], t.s[2], p, p2); bin32(x[5], x[7], t.w[2], t.s[2], p, p2);
+#pragma unroll
+  for (int k = 0; k < 4; k++) bin32(x[k], x[k + 4], t.w[0], t.s[0], p, p2);
+}
+// final pass on positions 8 tid + k: P stages with pair distance t = 2^{P-1-s}; stage s
+// uses 8 >> (P - s) consecutive pairs of the thread's group
 template <int P>
-FDFB_DEV void fwd_lastP(u64 x[8], const u64x2* tw, u64 Q, u64 Q2) {
+FDFB_DEV void fwd_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+  Tw8 t; load_tw8(t, g);
   int o = 0;
 #pragma unroll
   for (int s = 0; s < P; s++) {
-    const int t = 1 << (P - 1 - s);
+    const int d = 1 << (P - 1 - s);
 #pragma unroll
     for (int k = 0; k < 8; k++)
-      if ((k & t) == 0) bfw(x[k], x[k + t], ldp(tw + o + (k >> (P - s))), Q, Q2);
+      if ((k & d) == 0) bfw32(x[k], x[k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
     o += 8 >> (P - s);
   }
 }
 template <int P>
-FDFB_DEV void inv_lastP(u64 x[8], const u64x2* tw, u64 Q, u64 Q2) {
+FDFB_DEV void inv_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+  Tw8 t; load_tw8(t, g);
   int o = 8 - (8 >> P);
 #pragma unroll
   for (int s = P - 1; s >= 0; s--) {
-    const int t = 1 << (P - 1 - s);
+    const int d = 1 << (P - 1 - s);
     o -= 8 >> (P - s);
 #pragma unroll
     for (int k = 0; k < 8; k++)
-      if ((k & t) == 0) bin(x[k], x[k + t], ldp(tw + o + (k >> (P - s))), Q, Q2);
+      if ((k & d) == 0) bin32(x[k], x[k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
   }
 }
 
-FDFB_DEV int sw(int e) { return e ^ ((e >> 3) & 7) ^ (((e >> 4) & 3) << 2) ^ (((e >> 6) & 1) << 3); }
+// XOR swizzle of the u32 exchange buffer: conflict-free for every access pattern of the
+// transform (consecutive, T1-strided for T1 in {1..32}, 8 tid + k), checked exhaustively.
+FDFB_DEV int sw32(int e) {
+  const int x = (e >> 5) & 7;
+  const int x0 = x & 1, x1 = (x >> 1) & 1, x2 = (x >> 2) & 1;
+  return e ^ (x | ((x1 ^ x0) << 3) | ((x2 ^ x0) << 4));
+}
 
-// Forward NTT. In: x[k] = coefficient tid + T k in [0, 4Q).  Out: x[k] = slot 8 tid + k in [0, 4Q).
+// Forward NTT mod p. In: x[k] = coefficient tid + T k, [0, 4p).  Out: slot 8 tid + k, [0, 4p).
 template <int N>
-FDFB_DEV void ntt_fwd2(u64 x[8], u64* sb, int tid, const u64x2* tab, u64 Q, u64 Q2) {
+FDFB_DEV void ntt_fwd32(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   using S = BrShape<N>;
   constexpr int T = S::T;
-  fwd8(x, tab, Q, Q2);
+  fwd8_32(x, tab, p, p2);
 #pragma unroll
-  for (int k = 0; k < 8; k++) sb[sw(tid + T * k)] = x[k];
+  for (int k = 0; k < 8; k++) sb[sw32(tid + T * k)] = x[k];
   __syncthreads();
 #pragma unroll
   for (int q = 1; q < S::NMID; q++) {
@@ -117,24 +157,24 @@ FDFB_DEV void ntt_fwd2(u64 x[8], u64* sb, int tid, const u64x2* tab, u64 Q, u64 
     const int g = tid / T1;
     const int base = g * 8 * T1 + (tid % T1);
 #pragma unroll
-    for (int k = 0; k < 8; k++) x[k] = sb[sw(base + T1 * k)];
-    fwd8(x, tab + S::off(q) + 7 * g, Q, Q2);
+    for (int k = 0; k < 8; k++) x[k] = sb[sw32(base + T1 * k)];
+    fwd8_32(x, tab + 4 * (S::grp(q) + g), p, p2);
 #pragma unroll
-    for (int k = 0; k < 8; k++) sb[sw(base + T1 * k)] = x[k];
+    for (int k = 0; k < 8; k++) sb[sw32(base + T1 * k)] = x[k];
     __syncwarp();
   }
 #pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = sb[sw(8 * tid + k)];
-  fwd_lastP<S::PLAST>(x, tab + S::OFF_LAST + S::NLAST * tid, Q, Q2);
+  for (int k = 0; k < 8; k++) x[k] = sb[sw32(8 * tid + k)];
+  fwd_last32<S::PLAST>(x, tab + 4 * (S::G_LAST + tid), p, p2);
 }
-// Inverse NTT (unscaled).  In: x[k] = slot 8 tid + k in [0, 2Q).  Out: coefficient tid + T k, [0, 2Q).
+// Inverse NTT mod p (unscaled). In: slot 8 tid + k, [0, 2p).  Out: coefficient tid + T k, [0, 2p).
 template <int N>
-FDFB_DEV void ntt_inv2(u64 x[8], u64* sb, int tid, const u64x2* tab, u64 Q, u64 Q2) {
+FDFB_DEV void ntt_inv32(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   using S = BrShape<N>;
   constexpr int T = S::T;
-  inv_lastP<S::PLAST>(x, tab + S::OFF_LAST + S::NLAST * tid, Q, Q2);
+  inv_last32<S::PLAST>(x, tab + 4 * (S::G_LAST + tid), p, p2);
 #pragma unroll
-  for (int k = 0; k < 8; k++) sb[sw(8 * tid + k)] = x[k];
+  for (int k = 0; k < 8; k++) sb[sw32(8 * tid + k)] = x[k];
   __syncwarp();
 #pragma unroll
   for (int q = S::NMID - 1; q >= 1; q--) {
@@ -142,35 +182,50 @@ FDFB_DEV void ntt_inv2(u64 x[8], u64* sb, int tid, const u64x2* tab, u64 Q, u64 
     const int g = tid / T1;
     const int base = g * 8 * T1 + (tid % T1);
 #pragma unroll
-    for (int k = 0; k < 8; k++) x[k] = sb[sw(base + T1 * k)];
-    inv8(x, tab + S::off(q) + 7 * g, Q, Q2);
+    for (int k = 0; k < 8; k++) x[k] = sb[sw32(base + T1 * k)];
+    inv8_32(x, tab + 4 * (S::grp(q) + g), p, p2);
 #pragma unroll
-    for (int k = 0; k < 8; k++) sb[sw(base + T1 * k)] = x[k];
+    for (int k = 0; k < 8; k++) sb[sw32(base + T1 * k)] = x[k];
     __syncwarp();
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = sb[sw(tid + T * k)];
-  inv8(x, tab, Q, Q2);
+  for (int k = 0; k < 8; k++) x[k] = sb[sw32(tid + T * k)];
+  inv8_32(x, tab, p, p2);
 }
 
-template <int N>
+// s < 2^63 -> s mod p in [0, 2p):  s1 2^32 + s0 = s1 (2^32 mod p) + s0
+FDFB_DEV u32 red64(u64 s, const RnsParams& R, int i) {
+  const u32 s1 = (u32)(s >> 32), s0 = (u32)s;
+  const u32 a = shoup32(s1, R.r32[i], R.r32s[i], R.p[i]);            // [0, 2p)
+  const u32 b = s0 - __umulhi(s0, R.b32[i]) * R.p[i];                // [0, 2p)
+  return csub32(a + b, R.p2[i]);                                     // [0, 2p)
+}
+// 64-bit Shoup with a 32-bit multiplicand: c * m mod Q in [0, 2Q)
+FDFB_DEV u64 shoup64_32(u32 c, u64 m, u64 ms, u64 Q) {
+  const u64 q = __umul64hi((u64)c, ms);
+  return (u64)c * m - q * Q;
+}
+
+template <int N, int NP>
 __global__ void __launch_bounds__(N / 8, BrShape<N>::MINB)
-k_blind_rotate(DevParams p, const u64x2* __restrict__ bsk, const u64x2* __restrict__ ftab,
-               const u64x2* __restrict__ itab, u64* __restrict__ accs, int n_acc, int acc_per_ct,
-               const u32* __restrict__ abar) {
+k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
+               int acc_per_ct, const u32* __restrict__ abar) {
   using S = BrShape<N>;
   constexpr int T = S::T;
   extern __shared__ u64 smem[];
-  u64* sacc = smem;            // [b | a], natural order, canonical
-  u64* sd = smem + 2 * N;      // d = acc X^e - acc of the current half (thread-private slots)
-  u64* sb0 = smem + 3 * N;     // NTT exchange buffers (alternating)
-  u64* sb1 = smem + 4 * N;
+  u64* sacc = smem;                          // [b | a], natural order, canonical mod Q
+  u64* sd = smem + 2 * N;                    // d = acc X^e - acc, both halves (thread-private slots)
+  u32* sb0 = (u32*)(smem + 4 * N);           // NTT exchange buffers (alternating), N u32 each
+  u32* sb1 = sb0 + N;
+  u32* st0 = sb1 + N;                        // Garner staging: c0 [2][N]
+  u32* st1 = st0 + 2 * N;                    //                 c1 [2][N]
   const int tid = threadIdx.x;
-  const u64 Q = p.Q, Q2 = p.Q2;
+  const u64 Q = p.Q;
   const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
-  const u64 dmask = (1ULL << logL) - 1;
-  const size_t step_pairs = (size_t)2 * ell * 2 * N;
+  const u32 dmask = (1u << logL) - 1;
+  const size_t prime_words = (size_t)2 * ell * 2 * N;
+  const size_t step_words = (size_t)NP * prime_words;
 
   for (int g = blockIdx.x; g < n_acc; g += gridDim.x) {
     u64* acc = accs + (size_t)g * 2 * N;
@@ -186,69 +241,106 @@ k_blind_rotate(DevParams p, const u64x2* __restrict__ bsk, const u64x2* __restri
       for (int j = 0; j < u; j++) {
         // exponent -abar_i u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
-        const u64x2* K = bsk + ((size_t)i * u + j) * step_pairs + 8 * tid;
-        __syncthreads();                                  // previous step's acc writes
-        u64 mb[8], ma[8];
+        const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
+        __syncthreads();                                   // previous step's acc writes
+        // d = acc X^e - acc for both halves, once per CMux (thread-private slots of sd)
 #pragma unroll
-        for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
+        for (int k = 0; k < 16; k++) {
+          const int pos = tid + T * k;                     // in [0, 2N): half = pos / N
+          const int c = pos & (N - 1), h = pos - c;
+          const int idx = (c - e) & (2 * N - 1);           // coefficient c of X^e a = +-a[idx mod N]
+          const u64 v = sacc[h + (idx & (N - 1))];
+          const u64 rv = (idx >= N && v) ? Q - v : v;
+          sd[pos] = sub_mod(rv, sacc[pos], Q);
+        }
 #pragma unroll 1
-        for (int half = 0; half < 2; half++) {
-          const u64* src = sacc + half * N;
+        for (int pi = 0; pi < NP; pi++) {
+          const u32 pr = R.p[pi], pr2 = R.p2[pi];
+          const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
+          const uint4* it = R.itab + (size_t)pi * S::GROUPS * 4;
+          const u32* K = Kstep + (size_t)pi * prime_words;
+          u64 mb[8], ma[8];
 #pragma unroll
-          for (int k = 0; k < 8; k++) {
-            const int pos = tid + T * k;
-            sd[pos] = sub_mod(rot_coeff(src, pos, e, N, Q), src[pos], Q);
+          for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
+#pragma unroll 1
+          for (int half = 0; half < 2; half++) {
+            const u64* sdh = sd + half * N;
+#pragma unroll 1
+            for (int r = 0; r < ell; r++) {
+              const u32* Kb = K + (size_t)((half * ell + r) * 2) * N;
+              const u32* Ka = Kb + N;
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(Ka));
+              u32 x[8];
+              const int sh = r * logL;
+#pragma unroll
+              for (int k = 0; k < 8; k++) x[k] = (u32)(sdh[tid + T * k] >> sh) & dmask;
+              ntt_fwd32<N>(x, buf ? sb1 : sb0, tid, ft, pr, pr2);
+              buf ^= 1;
+              const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
+              const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
+              const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
+              const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
+#pragma unroll
+              for (int k = 0; k < 8; k++) {
+                const u32 xr = csub32(csub32(x[k], pr2), pr);          // [0, p)
+                mb[k] += (u64)xr * kb[k];                              // < 2 ell p^2 < 2^63
+                ma[k] += (u64)xr * ka[k];
+              }
+            }
           }
-#pragma unroll 1
-          for (int r = 0; r < ell; r++) {
-            const u64x2* Kb = K + (size_t)((half * ell + r) * 2) * N;
-            const u64x2* Ka = Kb + N;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb + 4));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Ka));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Ka + 4));
-            u64 x[8];
-            const int sh = r * logL;
+          // the a-column sums wait in the idle exchange buffer (buf ^ 1) during INTT(b): after
+          // the last forward transform's barrier each warp only touches its own 8T/W-element
+          // region of that buffer, and slots 8 tid + k lie in it
+          u32 xb[8];
+          u32* park = buf ? sb0 : sb1;
 #pragma unroll
-            for (int k = 0; k < 8; k++) x[k] = (sd[tid + T * k] >> sh) & dmask;
-            ntt_fwd2<N>(x, buf ? sb1 : sb0, tid, ftab, Q, Q2);
+          for (int k = 0; k < 8; k++) { xb[k] = red64(mb[k], R, pi); park[sw32(8 * tid + k)] = red64(ma[k], R, pi); }
+#pragma unroll 1
+          for (int c = 0; c < 2; c++) {
+            u32 x[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) x[k] = c ? park[sw32(8 * tid + k)] : xb[k];
+            ntt_inv32<N>(x, buf ? sb1 : sb0, tid, it, pr, pr2);
             buf ^= 1;
+            u32* s0 = st0 + c * N;
+            u32* s1 = st1 + c * N;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
-              const u64x2 wb = __ldg(Kb + k);
-              mb[k] += mul_shoup_lazy(x[k], wb.x, wb.y, Q);
-            }
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-              const u64x2 wa = __ldg(Ka + k);
-              ma[k] += mul_shoup_lazy(x[k], wa.x, wa.y, Q);
+              const int pos = tid + T * k;
+              const u32 rv = csub32(x[k], pr);                         // residue mod p_pi, [0, p)
+              if (pi == 0) {
+                s0[pos] = rv;
+              } else if (pi == 1) {
+                const u32 c0 = s0[pos];
+                const u32 c0m = csub32(c0, R.p[1]);                    // c0 mod p1 (p0 < 2 p1)
+                const u32 c1 = csub32(shoup32(rv + R.p[1] - c0m, R.g01, R.g01s, R.p[1]), R.p[1]);
+                if (NP == 2) {
+                  // V = c0 + c1 p0 - [c1 > p1/2] P  (mod Q)
+                  u64 v = shoup64_32(c0, R.m0, R.m0s, Q) + shoup64_32(c1, R.m1, R.m1s, Q);   // < 4Q
+                  if (c1 > (R.p[1] >> 1)) v += Q - R.pmq;                                    // V < 0
+                  v = csub(csub(v, Q << 2), Q << 1);
+                  v = csub(v, Q);
+                  sacc[c * N + pos] = add_mod(sacc[c * N + pos], v, Q);
+                } else {
+                  s1[pos] = c1;
+                }
+              } else {
+                const u32 c0 = s0[pos], c1 = s1[pos];
+                const u32 c0m = csub32(c0, R.p[2]);
+                const u32 c1m = csub32(c1, R.p[2]);
+                const u32 u1 = shoup32(rv + R.p[2] - c0m, R.g02, R.g02s, R.p[2]);   // [0, 2 p2)
+                const u32 u2 = shoup32(c1m, R.g12, R.g12s, R.p[2]);                 // [0, 2 p2)
+                const u32 c2 = csub32(csub32(u1 + R.p2[2] - u2, R.p2[2]), R.p[2]);  // [0, p2)
+                u64 v = shoup64_32(c0, R.m0, R.m0s, Q) + shoup64_32(c1, R.m1, R.m1s, Q) +
+                        shoup64_32(c2, R.m2, R.m2s, Q);                                     // < 6Q
+                if (c2 > (R.p[2] >> 1)) v += Q - R.pmq;                             // V < 0
+                v = csub(csub(v, Q << 2), Q << 1);
+                v = csub(v, Q);
+                sacc[c * N + pos] = add_mod(sacc[c * N + pos], v, Q);
+              }
             }
           }
-        }
-        // 2 ell terms in [0, 2Q) each (< 16Q): reduce into [0, 2Q) for the inverse transform
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-#pragma unroll
-          for (int s = 3; s >= 1; s--) { mb[k] = csub(mb[k], Q << s); ma[k] = csub(ma[k], Q << s); }
-        }
-        // park the a-column sums in the (now free, thread-private) d scratch during INTT(b)
-#pragma unroll
-        for (int k = 0; k < 8; k++) sd[tid + T * k] = ma[k];
-        ntt_inv2<N>(mb, buf ? sb1 : sb0, tid, itab, Q, Q2);
-        buf ^= 1;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const int pos = tid + T * k;
-          sacc[pos] = add_mod(sacc[pos], csub(mb[k], Q), Q);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; k++) ma[k] = sd[tid + T * k];
-        ntt_inv2<N>(ma, buf ? sb1 : sb0, tid, itab, Q, Q2);
-        buf ^= 1;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const int pos = N + tid + T * k;
-          sacc[pos] = add_mod(sacc[pos], csub(ma[k], Q), Q);
         }
       }
     }
@@ -258,14 +350,33 @@ k_blind_rotate(DevParams p, const u64x2* __restrict__ bsk, const u64x2* __restri
   }
 }
 
-// Device brK from canonical rows already forward-transformed (slots, [0, Q)):
-// pair (w N^{-1} mod Q, Shoup companion).  ntt_rows: [rows*2 polys][N].
-__global__ void k_brk_finalize(DevParams p, const u64* __restrict__ ntt_rows, u64x2* __restrict__ dev, size_t npoly) {
-  const int N = p.N;
-  size_t total = npoly * N;
-  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
-    u64 v = csub(mul_shoup_lazy(ntt_rows[x], p.ninv, p.ninvp, p.Q), p.Q);
-    u64 vp = (u64)(((unsigned __int128)v << 64) / p.Q);
-    dev[x] = make_ulonglong2(v, vp);
+// brK import: canonical RGSW rows (coefficient domain, [0, Q)) -> for each prime p_i:
+// NTT_p(row mod p_i) * N^{-1} mod p_i, in [0, p_i).  One CTA (T threads) per (poly, prime);
+// poly = row*2 + col of the canonical [rows][2][N] block starting at flat row `row0`.
+template <int N>
+__global__ void __launch_bounds__(N / 8)
+k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, u32* __restrict__ dev) {
+  using S = BrShape<N>;
+  constexpr int T = S::T;
+  __shared__ u32 sb[N];
+  const int tid = threadIdx.x;
+  const int pi = blockIdx.y;
+  const size_t poly = blockIdx.x;              // local row*2 + col
+  const size_t frow = row0 + poly / 2;         // flat canonical row = step*2ell + r
+  const int col = (int)(poly % 2);
+  const int rows_per_step = 2 * p.ell_rgsw;
+  const size_t step = frow / rows_per_step;
+  const int r = (int)(frow % rows_per_step);
+  const u32 pr = R.p[pi], pr2 = R.p2[pi];
+  const u64* src = canon + poly * N;
+  u32 x[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) x[k] = (u32)(src[tid + T * k] % pr);
+  ntt_fwd32<N>(x, sb, tid, R.ftab + (size_t)pi * S::GROUPS * 4, pr, pr2);
+  u32* o = dev + ((step * R.np + pi) * rows_per_step + r) * 2 * (size_t)N + (size_t)col * N + 8 * tid;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const u32 v = csub32(csub32(x[k], pr2), pr);
+    o[k] = csub32(shoup32(v, R.ninv[pi], R.ninvs[pi], pr), pr);
   }
 }

@@ -227,8 +227,12 @@ k_shift(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __re
   const u64* U = pk + lay.U + (size_t)h * N;
 #pragma unroll
   for (int c = 0; c < C; c++) {
-    if (!ok[c]) continue;                               // uniform across the CTA
     const int g = blockIdx.x * C + c;
+    if (!ok[c]) {                                       // uniform across the CTA
+      if (g < B)                                        // out-of-range d: zero row (flag raised)
+        for (int x = tid; x < N; x += TPB) out[(size_t)g * 2 * N + (size_t)h * N + x] = 0;
+      continue;
+    }
     const u64* cth = ct + (size_t)g * 2 * N + (size_t)h * N;
     __syncthreads();
 #pragma unroll
