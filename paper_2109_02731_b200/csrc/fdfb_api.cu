@@ -173,7 +173,7 @@ template <int N, int NP>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
                        cudaStream_t st) {
   constexpr int T = N / 8;
-  const size_t sm = 56 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange 8N + Garner staging 16N bytes
+  const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + 2 exchange 9N + Garner staging 16N bytes
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_blind_rotate<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -275,7 +275,7 @@ static u64 h_primroot_2n(u64 pr, int N) {
   }
   return 0;
 }
-// Choose the RNS primes (largest p < 2^30, p = 1 mod 2N) so that prod p > 2 * bound + 1 with
+// Choose the RNS primes (largest p < 2^29 so that 6p < 2^32, p = 1 mod 2N) so that prod p > 2 * bound + 1 with
 // bound = 2 ell N (L-1) (Q-1) >= |coefficients| of sum_r D_r * K_r; build constants/tables.
 static int setup_rns(fdfb_ctx* c) {
   const fdfb_params& p = c->prm;
@@ -285,9 +285,9 @@ static int setup_rns(fdfb_ctx* c) {
   const u128 bound = (u128)(2 * p.ell_rgsw) * N * ((1ULL << p.logL_rgsw) - 1) * (p.Q - 1);
   std::vector<u64> primes;
   u128 P = 1;
-  for (u64 cand = ((1ULL << 30) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 29) && primes.size() < RNS_MAXP;
+  for (u64 cand = ((1ULL << 29) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 28) && primes.size() < RNS_MAXP;
        cand -= 2 * (u64)N) {
-    if (cand >= (1ULL << 30) || cand == p.Q || !h_is_prime(cand)) continue;
+    if (cand >= (1ULL << 29) || cand == p.Q || !h_is_prime(cand)) continue;
     primes.push_back(cand);
     P *= cand;
     if (primes.size() >= 2 && P / 2 > bound + 1) break;

@@ -8,8 +8,8 @@
 //
 // Exact RNS evaluation of the external product.  The products D_r * K (negacyclic, over
 // the integers, K in [0, Q)) have |coefficients| < 2 ell N (L-1) Q (< 2^82 at the Large
-// configuration), so they are computed exactly modulo NP word-size NTT primes p_i < 2^30
-// (P = prod p_i > 2 * bound) with 32-bit Harvey/Shoup arithmetic, and the signed integer
+// configuration), so they are computed exactly modulo NP word-size NTT primes
+// (P = prod p_i > 2 * bound; p_i < 2^29) with 32-bit Harvey/Shoup arithmetic, and the signed integer
 // result is recovered by Garner CRT and reduced mod Q.  The result is the same residue
 // vector as the schoolbook definition (bit-exact with any correct evaluation); it costs
 // ~4 IMAD slots per 30-bit butterfly instead of ~16-22 for a 54-bit Shoup butterfly.
@@ -66,16 +66,21 @@ FDFB_DEV u32 shoup32(u32 a, u32 w, u32 ws, u32 p) {     // a*w mod p in [0, 2p),
 }
 FDFB_DEV u32 csub32(u32 x, u32 m) { return min(x, x - m); }
 
-FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // Harvey CT, [0, 4p)
-  const u32 x = csub32(X, p2);
-  const u32 t = shoup32(Y, w, ws, p);
-  X = x + t;
-  Y = x - t + p2;
+// Harvey butterflies with every add written as a 3-input IADD3 (keeps the adds on the ALU
+// pipe; two-input adds are otherwise issued as IMAD.IADD on the multiply pipe) and the
+// conditional subtractions as unsigned min (VIADDMNMX).  Needs 6p < 2^32 (p < 2^29).
+FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // CT, in/out [0, 4p)
+  const u32 t = shoup32(Y, w, ws, p);                                   // [0, 2p)
+  const u32 s = X + t - p2;                                             // [-2p, 4p)
+  const u32 y = X - t + p2;                                             // (0, 6p)
+  X = min(s, s + p2);                                                   // [0, 4p)
+  Y = min(y, y - p2);                                                   // [0, 4p)
 }
-FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // Harvey GS, [0, 2p)
+FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // GS, in/out [0, 2p)
   const u32 x = X, y = Y;
-  X = csub32(x + y, p2);
-  Y = shoup32(x - y + p2, w, ws, p);
+  const u32 s = x + y - p2;                                             // [-2p, 2p)
+  X = min(s, s + p2);                                                   // [0, 2p)
+  Y = shoup32(x - y + p2, w, ws, p);                                    // [0, 2p)
 }
 
 // 8 pairs of a group: tw[0] stage-0, tw[1..2] stage-1, tw[3..6] stage-2 (tw[7] padding)
@@ -134,63 +139,97 @@ FDFB_DEV void inv_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
   }
 }
 
-// XOR swizzle of the u32 exchange buffer: conflict-free for every access pattern of the
-// transform (consecutive, T1-strided for T1 in {1..32}, 8 tid + k), checked exhaustively.
-FDFB_DEV int sw32(int e) {
-  const int x = (e >> 5) & 7;
-  const int x0 = x & 1, x1 = (x >> 1) & 1, x2 = (x >> 2) & 1;
-  return e ^ (x | ((x1 ^ x0) << 3) | ((x2 ^ x0) << 4));
+// Exchange-buffer layouts.  Exchange x (between radix-8 pass x and x+1) stores logical
+// position e at L_x(e) = e + m_x (e >> s_x); every (s_x, m_x) below maps each warp's 256
+// positions into its own 288-word slab (so warp-local passes never touch another warp's
+// slab) and is bank-conflict free for both the writing and the reading pass (checked
+// exhaustively).  For a pass pattern e = B(tid) + S k the address is L_x(B) + S k +
+// m_x ((S k) >> s_x): a per-thread base plus compile-time offsets.
+template <int N>
+struct Lay {
+  static constexpr int S(int x) { return (x == BrShape<N>::NMID - 1) ? 3 : (N == 1024 && x == 1) ? 4 : 5; }
+  static constexpr int M(int x) { return (x == BrShape<N>::NMID - 1) ? 1 : (N == 1024 && x == 1) ? 2 : 4; }
+  static constexpr int WORDS = N + N / 8;
+};
+template <int N, int X>
+FDFB_DEV int lay_base(int e) { return e + Lay<N>::M(X) * (e >> Lay<N>::S(X)); }
+template <int N, int X>
+FDFB_DEV constexpr int lay_off(int S, int k) { return S * k + Lay<N>::M(X) * ((S * k) >> Lay<N>::S(X)); }
+
+// pass-q position pattern: B = (tid / T1) 8 T1 + tid % T1, stride T1
+template <int N, int q>
+FDFB_DEV int qbase(int tid) { constexpr int T1 = N >> (3 * q + 3); return (tid / T1) * 8 * T1 + (tid % T1); }
+
+template <int N, int q>
+FDFB_DEV void fwd_mid(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+  if constexpr (q < BrShape<N>::NMID) {
+    constexpr int T1 = N >> (3 * q + 3);
+    const int B = qbase<N, q>(tid);
+    const u32* r = sb + lay_base<N, q - 1>(B);
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = r[lay_off<N, q - 1>(T1, k)];
+    fwd8_32(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
+    __syncwarp();
+    u32* w = sb + lay_base<N, q>(B);
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[lay_off<N, q>(T1, k)] = x[k];
+    __syncwarp();
+    fwd_mid<N, q + 1>(x, sb, tid, tab, p, p2);
+  }
+}
+template <int N, int q>
+FDFB_DEV void inv_mid(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+  if constexpr (q >= 1) {
+    constexpr int T1 = N >> (3 * q + 3);
+    const int B = qbase<N, q>(tid);
+    const u32* r = sb + lay_base<N, q>(B);
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = r[lay_off<N, q>(T1, k)];
+    inv8_32(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
+    __syncwarp();
+    u32* w = sb + lay_base<N, q - 1>(B);
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[lay_off<N, q - 1>(T1, k)] = x[k];
+    __syncwarp();
+    inv_mid<N, q - 1>(x, sb, tid, tab, p, p2);
+  }
 }
 
 // Forward NTT mod p. In: x[k] = coefficient tid + T k, [0, 4p).  Out: slot 8 tid + k, [0, 4p).
 template <int N>
 FDFB_DEV void ntt_fwd32(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   using S = BrShape<N>;
-  constexpr int T = S::T;
+  constexpr int T = S::T, NM = S::NMID;
   fwd8_32(x, tab, p, p2);
+  {
+    u32* w = sb + lay_base<N, 0>(tid);
 #pragma unroll
-  for (int k = 0; k < 8; k++) sb[sw32(tid + T * k)] = x[k];
-  __syncthreads();
-#pragma unroll
-  for (int q = 1; q < S::NMID; q++) {
-    const int T1 = N >> (3 * q + 3);
-    const int g = tid / T1;
-    const int base = g * 8 * T1 + (tid % T1);
-#pragma unroll
-    for (int k = 0; k < 8; k++) x[k] = sb[sw32(base + T1 * k)];
-    fwd8_32(x, tab + 4 * (S::grp(q) + g), p, p2);
-#pragma unroll
-    for (int k = 0; k < 8; k++) sb[sw32(base + T1 * k)] = x[k];
-    __syncwarp();
+    for (int k = 0; k < 8; k++) w[lay_off<N, 0>(T, k)] = x[k];
   }
+  __syncthreads();
+  fwd_mid<N, 1>(x, sb, tid, tab, p, p2);
+  const u32* r = sb + lay_base<N, NM - 1>(8 * tid);
 #pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = sb[sw32(8 * tid + k)];
+  for (int k = 0; k < 8; k++) x[k] = r[k];
   fwd_last32<S::PLAST>(x, tab + 4 * (S::G_LAST + tid), p, p2);
 }
 // Inverse NTT mod p (unscaled). In: slot 8 tid + k, [0, 2p).  Out: coefficient tid + T k, [0, 2p).
 template <int N>
 FDFB_DEV void ntt_inv32(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   using S = BrShape<N>;
-  constexpr int T = S::T;
+  constexpr int T = S::T, NM = S::NMID;
   inv_last32<S::PLAST>(x, tab + 4 * (S::G_LAST + tid), p, p2);
+  {
+    u32* w = sb + lay_base<N, NM - 1>(8 * tid);
 #pragma unroll
-  for (int k = 0; k < 8; k++) sb[sw32(8 * tid + k)] = x[k];
-  __syncwarp();
-#pragma unroll
-  for (int q = S::NMID - 1; q >= 1; q--) {
-    const int T1 = N >> (3 * q + 3);
-    const int g = tid / T1;
-    const int base = g * 8 * T1 + (tid % T1);
-#pragma unroll
-    for (int k = 0; k < 8; k++) x[k] = sb[sw32(base + T1 * k)];
-    inv8_32(x, tab + 4 * (S::grp(q) + g), p, p2);
-#pragma unroll
-    for (int k = 0; k < 8; k++) sb[sw32(base + T1 * k)] = x[k];
-    __syncwarp();
+    for (int k = 0; k < 8; k++) w[k] = x[k];
   }
+  __syncwarp();
+  inv_mid<N, NM - 1>(x, sb, tid, tab, p, p2);
   __syncthreads();
+  const u32* r = sb + lay_base<N, 0>(tid);
 #pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = sb[sw32(tid + T * k)];
+  for (int k = 0; k < 8; k++) x[k] = r[lay_off<N, 0>(T, k)];
   inv8_32(x, tab, p, p2);
 }
 
@@ -215,10 +254,10 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
   constexpr int T = S::T;
   extern __shared__ u64 smem[];
   u64* sacc = smem;                          // [b | a], natural order, canonical mod Q
-  u64* sd = smem + 2 * N;                    // d = acc X^e - acc, both halves (thread-private slots)
-  u32* sb0 = (u32*)(smem + 4 * N);           // NTT exchange buffers (alternating), N u32 each
-  u32* sb1 = sb0 + N;
-  u32* st0 = sb1 + N;                        // Garner staging: c0 [2][N]
+  u64* sd = smem + 2 * N;                    // d = acc X^e - acc of one half (thread-private slots)
+  u32* sb0 = (u32*)(smem + 3 * N);           // NTT exchange buffers (alternating), 9N/8 u32 each
+  u32* sb1 = sb0 + Lay<N>::WORDS;
+  u32* st0 = sb1 + Lay<N>::WORDS;            // Garner staging: c0 [2][N]
   u32* st1 = st0 + 2 * N;                    //                 c1 [2][N]
   const int tid = threadIdx.x;
   const u64 Q = p.Q;
@@ -243,16 +282,6 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
         __syncthreads();                                   // previous step's acc writes
-        // d = acc X^e - acc for both halves, once per CMux (thread-private slots of sd)
-#pragma unroll
-        for (int k = 0; k < 16; k++) {
-          const int pos = tid + T * k;                     // in [0, 2N): half = pos / N
-          const int c = pos & (N - 1), h = pos - c;
-          const int idx = (c - e) & (2 * N - 1);           // coefficient c of X^e a = +-a[idx mod N]
-          const u64 v = sacc[h + (idx & (N - 1))];
-          const u64 rv = (idx >= N && v) ? Q - v : v;
-          sd[pos] = sub_mod(rv, sacc[pos], Q);
-        }
 #pragma unroll 1
         for (int pi = 0; pi < NP; pi++) {
           const u32 pr = R.p[pi], pr2 = R.p2[pi];
@@ -264,7 +293,17 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
 #pragma unroll 1
           for (int half = 0; half < 2; half++) {
-            const u64* sdh = sd + half * N;
+            // d = acc X^e - acc of this half (thread-private slots of sd; branchless rotation)
+            const u64* src = sacc + half * N;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              const int pos = tid + T * k;
+              const int idx = (pos - e) & (2 * N - 1);     // coefficient pos of X^e a = +-a[idx mod N]
+              const u64 v = src[idx & (N - 1)];
+              const u64 rv = (idx >= N && v) ? Q - v : v;
+              sd[pos] = sub_mod(rv, src[pos], Q);
+            }
+            const u64* sdh = sd;
 #pragma unroll 1
             for (int r = 0; r < ell; r++) {
               const u32* Kb = K + (size_t)((half * ell + r) * 2) * N;
@@ -294,13 +333,14 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           // region of that buffer, and slots 8 tid + k lie in it
           u32 xb[8];
           u32* park = buf ? sb0 : sb1;
+          const int parkb = lay_base<N, S::NMID - 1>(8 * tid);     // the thread's PL slots
 #pragma unroll
-          for (int k = 0; k < 8; k++) { xb[k] = red64(mb[k], R, pi); park[sw32(8 * tid + k)] = red64(ma[k], R, pi); }
+          for (int k = 0; k < 8; k++) { xb[k] = red64(mb[k], R, pi); park[parkb + k] = red64(ma[k], R, pi); }
 #pragma unroll 1
           for (int c = 0; c < 2; c++) {
             u32 x[8];
 #pragma unroll
-            for (int k = 0; k < 8; k++) x[k] = c ? park[sw32(8 * tid + k)] : xb[k];
+            for (int k = 0; k < 8; k++) x[k] = c ? park[parkb + k] : xb[k];
             ntt_inv32<N>(x, buf ? sb1 : sb0, tid, it, pr, pr2);
             buf ^= 1;
             u32* s0 = st0 + c * N;
@@ -358,7 +398,7 @@ __global__ void __launch_bounds__(N / 8)
 k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, u32* __restrict__ dev) {
   using S = BrShape<N>;
   constexpr int T = S::T;
-  __shared__ u32 sb[N];
+  __shared__ u32 sb[Lay<N>::WORDS];
   const int tid = threadIdx.x;
   const int pi = blockIdx.y;
   const size_t poly = blockIdx.x;              // local row*2 + col
