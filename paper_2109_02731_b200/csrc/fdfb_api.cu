@@ -173,7 +173,7 @@ template <int N, int NP>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
                        cudaStream_t st) {
   constexpr int T = N / 8;
-  const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + 2 exchange 9N + Garner staging 16N bytes
+  const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + exchange 2 planes 9N + Garner staging 16N bytes
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_blind_rotate<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -92,41 +92,66 @@ FDFB_DEV void load_tw8(Tw8& t, const uint4* g) {
     t.w[2 * i] = v.x; t.s[2 * i] = v.y; t.w[2 * i + 1] = v.z; t.s[2 * i + 1] = v.w;
   }
 }
-FDFB_DEV void fwd8_32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+// V polynomials (V = 1 or 2) share every twiddle: twice the ILP and half the twiddle
+// loads per polynomial when two digit (or two column) transforms run together.
+template <int V>
+FDFB_DEV void fwd8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
   Tw8 t; load_tw8(t, g);
 #pragma unroll
-  for (int k = 0; k < 4; k++) bfw32(x[k], x[k + 4], t.w[0], t.s[0], p, p2);
-  bfw32(x[0], x[2], t.w[1], t.s[1], p, p2); bfw32(x[1], x[3], t.w[1], t.s[1], p, p2);
-  bfw32(x[4], x[6], t.w[2], t.s[2], p, p2); bfw32(x[5], x[7], t.w[2], t.s[2], p, p2);
+  for (int v = 0; v < V; v++) {
 #pragma unroll
-  for (int k = 0; k < 4; k++) bfw32(x[2 * k], x[2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
+    for (int k = 0; k < 4; k++) bfw32(x[v][k], x[v][k + 4], t.w[0], t.s[0], p, p2);
+  }
+#pragma unroll
+  for (int v = 0; v < V; v++) {
+    bfw32(x[v][0], x[v][2], t.w[1], t.s[1], p, p2); bfw32(x[v][1], x[v][3], t.w[1], t.s[1], p, p2);
+    bfw32(x[v][4], x[v][6], t.w[2], t.s[2], p, p2); bfw32(x[v][5], x[v][7], t.w[2], t.s[2], p, p2);
+  }
+#pragma unroll
+  for (int v = 0; v < V; v++) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) bfw32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
+  }
 }
-FDFB_DEV void inv8_32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+template <int V>
+FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
   Tw8 t; load_tw8(t, g);
 #pragma unroll
-  for (int k = 0; k < 4; k++) bin32(x[2 * k], x[2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
-  bin32(x[0], x[2], t.w[1], t.s[1], p, p2); bin32(x[1], x[3], t.w[1], t.s[1], p, p2);
-  bin32(x[4], x[6], t.w[2], t.s[2], p, p2); bin32(x[5], x[7], t.w[2], t.s[2], p, p2);
+  for (int v = 0; v < V; v++) {
 #pragma unroll
-  for (int k = 0; k < 4; k++) bin32(x[k], x[k + 4], t.w[0], t.s[0], p, p2);
+    for (int k = 0; k < 4; k++) bin32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
+  }
+#pragma unroll
+  for (int v = 0; v < V; v++) {
+    bin32(x[v][0], x[v][2], t.w[1], t.s[1], p, p2); bin32(x[v][1], x[v][3], t.w[1], t.s[1], p, p2);
+    bin32(x[v][4], x[v][6], t.w[2], t.s[2], p, p2); bin32(x[v][5], x[v][7], t.w[2], t.s[2], p, p2);
+  }
+#pragma unroll
+  for (int v = 0; v < V; v++) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) bin32(x[v][k], x[v][k + 4], t.w[0], t.s[0], p, p2);
+  }
 }
 // final pass on positions 8 tid + k: P stages with pair distance t = 2^{P-1-s}; stage s
 // uses 8 >> (P - s) consecutive pairs of the thread's group
-template <int P>
-FDFB_DEV void fwd_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+template <int P, int V>
+FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
   Tw8 t; load_tw8(t, g);
   int o = 0;
 #pragma unroll
   for (int s = 0; s < P; s++) {
     const int d = 1 << (P - 1 - s);
 #pragma unroll
-    for (int k = 0; k < 8; k++)
-      if ((k & d) == 0) bfw32(x[k], x[k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
+    for (int v = 0; v < V; v++) {
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if ((k & d) == 0) bfw32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
+    }
     o += 8 >> (P - s);
   }
 }
-template <int P>
-FDFB_DEV void inv_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
+template <int P, int V>
+FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
   Tw8 t; load_tw8(t, g);
   int o = 8 - (8 >> P);
 #pragma unroll
@@ -134,8 +159,11 @@ FDFB_DEV void inv_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
     const int d = 1 << (P - 1 - s);
     o -= 8 >> (P - s);
 #pragma unroll
-    for (int k = 0; k < 8; k++)
-      if ((k & d) == 0) bin32(x[k], x[k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
+    for (int v = 0; v < V; v++) {
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if ((k & d) == 0) bin32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
+    }
   }
 }
 
@@ -144,7 +172,8 @@ FDFB_DEV void inv_last32(u32 x[8], const uint4* g, u32 p, u32 p2) {
 // positions into its own 288-word slab (so warp-local passes never touch another warp's
 // slab) and is bank-conflict free for both the writing and the reading pass (checked
 // exhaustively).  For a pass pattern e = B(tid) + S k the address is L_x(B) + S k +
-// m_x ((S k) >> s_x): a per-thread base plus compile-time offsets.
+// m_x ((S k) >> s_x): a per-thread base plus compile-time offsets.  V polynomials use V
+// planes of WORDS words.
 template <int N>
 struct Lay {
   static constexpr int S(int x) { return (x == BrShape<N>::NMID - 1) ? 3 : (N == 1024 && x == 1) ? 4 : 5; }
@@ -160,77 +189,74 @@ FDFB_DEV constexpr int lay_off(int S, int k) { return S * k + Lay<N>::M(X) * ((S
 template <int N, int q>
 FDFB_DEV int qbase(int tid) { constexpr int T1 = N >> (3 * q + 3); return (tid / T1) * 8 * T1 + (tid % T1); }
 
-template <int N, int q>
-FDFB_DEV void fwd_mid(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+template <int N, int X, int V>
+FDFB_DEV void xload(u32 (&x)[V][8], const u32* sb, int base, int S) {
+#pragma unroll
+  for (int v = 0; v < V; v++)
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[v][k] = sb[v * Lay<N>::WORDS + base + lay_off<N, X>(S, k)];
+}
+template <int N, int X, int V>
+FDFB_DEV void xstore(const u32 (&x)[V][8], u32* sb, int base, int S) {
+#pragma unroll
+  for (int v = 0; v < V; v++)
+#pragma unroll
+    for (int k = 0; k < 8; k++) sb[v * Lay<N>::WORDS + base + lay_off<N, X>(S, k)] = x[v][k];
+}
+
+template <int N, int q, int V>
+FDFB_DEV void fwd_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   if constexpr (q < BrShape<N>::NMID) {
     constexpr int T1 = N >> (3 * q + 3);
     const int B = qbase<N, q>(tid);
-    const u32* r = sb + lay_base<N, q - 1>(B);
-#pragma unroll
-    for (int k = 0; k < 8; k++) x[k] = r[lay_off<N, q - 1>(T1, k)];
-    fwd8_32(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
+    xload<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
+    fwd8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
     __syncwarp();
-    u32* w = sb + lay_base<N, q>(B);
-#pragma unroll
-    for (int k = 0; k < 8; k++) w[lay_off<N, q>(T1, k)] = x[k];
+    xstore<N, q, V>(x, sb, lay_base<N, q>(B), T1);
     __syncwarp();
-    fwd_mid<N, q + 1>(x, sb, tid, tab, p, p2);
+    fwd_mid<N, q + 1, V>(x, sb, tid, tab, p, p2);
   }
 }
-template <int N, int q>
-FDFB_DEV void inv_mid(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+template <int N, int q, int V>
+FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   if constexpr (q >= 1) {
     constexpr int T1 = N >> (3 * q + 3);
     const int B = qbase<N, q>(tid);
-    const u32* r = sb + lay_base<N, q>(B);
-#pragma unroll
-    for (int k = 0; k < 8; k++) x[k] = r[lay_off<N, q>(T1, k)];
-    inv8_32(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
+    xload<N, q, V>(x, sb, lay_base<N, q>(B), T1);
+    inv8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
     __syncwarp();
-    u32* w = sb + lay_base<N, q - 1>(B);
-#pragma unroll
-    for (int k = 0; k < 8; k++) w[lay_off<N, q - 1>(T1, k)] = x[k];
+    xstore<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
     __syncwarp();
-    inv_mid<N, q - 1>(x, sb, tid, tab, p, p2);
+    inv_mid<N, q - 1, V>(x, sb, tid, tab, p, p2);
   }
 }
 
-// Forward NTT mod p. In: x[k] = coefficient tid + T k, [0, 4p).  Out: slot 8 tid + k, [0, 4p).
-template <int N>
-FDFB_DEV void ntt_fwd32(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+// Forward NTT mod p of V polynomials. In: x[v][k] = coefficient tid + T k, [0, 4p).
+// Out: slot 8 tid + k, [0, 4p).  The caller guarantees that no thread still reads sb.
+template <int N, int V>
+FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   using S = BrShape<N>;
   constexpr int T = S::T, NM = S::NMID;
-  fwd8_32(x, tab, p, p2);
-  {
-    u32* w = sb + lay_base<N, 0>(tid);
-#pragma unroll
-    for (int k = 0; k < 8; k++) w[lay_off<N, 0>(T, k)] = x[k];
-  }
+  fwd8_32<V>(x, tab, p, p2);
+  xstore<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
   __syncthreads();
-  fwd_mid<N, 1>(x, sb, tid, tab, p, p2);
-  const u32* r = sb + lay_base<N, NM - 1>(8 * tid);
-#pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = r[k];
-  fwd_last32<S::PLAST>(x, tab + 4 * (S::G_LAST + tid), p, p2);
+  fwd_mid<N, 1, V>(x, sb, tid, tab, p, p2);
+  xload<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
+  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2);
 }
-// Inverse NTT mod p (unscaled). In: slot 8 tid + k, [0, 2p).  Out: coefficient tid + T k, [0, 2p).
-template <int N>
-FDFB_DEV void ntt_inv32(u32 x[8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+// Inverse NTT mod p (unscaled) of V polynomials. In: slot 8 tid + k, [0, 2p).  Out:
+// coefficient tid + T k, [0, 2p).  Starts warp-locally; ends after a CTA barrier.
+template <int N, int V>
+FDFB_DEV void ntt_inv32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
   using S = BrShape<N>;
   constexpr int T = S::T, NM = S::NMID;
-  inv_last32<S::PLAST>(x, tab + 4 * (S::G_LAST + tid), p, p2);
-  {
-    u32* w = sb + lay_base<N, NM - 1>(8 * tid);
-#pragma unroll
-    for (int k = 0; k < 8; k++) w[k] = x[k];
-  }
+  inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2);
+  xstore<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
   __syncwarp();
-  inv_mid<N, NM - 1>(x, sb, tid, tab, p, p2);
+  inv_mid<N, NM - 1, V>(x, sb, tid, tab, p, p2);
   __syncthreads();
-  const u32* r = sb + lay_base<N, 0>(tid);
-#pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = r[lay_off<N, 0>(T, k)];
-  inv8_32(x, tab, p, p2);
+  xload<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
+  inv8_32<V>(x, tab, p, p2);
 }
 
 // s < 2^63 -> s mod p in [0, 2p):  s1 2^32 + s0 = s1 (2^32 mod p) + s0
@@ -255,9 +281,8 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
   extern __shared__ u64 smem[];
   u64* sacc = smem;                          // [b | a], natural order, canonical mod Q
   u64* sd = smem + 2 * N;                    // d = acc X^e - acc of one half (thread-private slots)
-  u32* sb0 = (u32*)(smem + 3 * N);           // NTT exchange buffers (alternating), 9N/8 u32 each
-  u32* sb1 = sb0 + Lay<N>::WORDS;
-  u32* st0 = sb1 + Lay<N>::WORDS;            // Garner staging: c0 [2][N]
+  u32* sb = (u32*)(smem + 3 * N);            // NTT exchange buffer: 2 planes of 9N/8 words
+  u32* st0 = sb + 2 * Lay<N>::WORDS;         // Garner staging: c0 [2][N]
   u32* st1 = st0 + 2 * N;                    //                 c1 [2][N]
   const int tid = threadIdx.x;
   const u64 Q = p.Q;
@@ -272,7 +297,6 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
     for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
     const u32* ab = abar + (size_t)(g / acc_per_ct) * p.n;
-    int buf = 0;
 #pragma unroll 1
     for (int i = 0; i < p.n; i++) {
       const u32 ai = __ldg(ab + i);
@@ -281,7 +305,6 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
         // exponent -abar_i u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
-        __syncthreads();                                   // previous step's acc writes
 #pragma unroll 1
         for (int pi = 0; pi < NP; pi++) {
           const u32 pr = R.p[pi], pr2 = R.p2[pi];
@@ -293,6 +316,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
 #pragma unroll 1
           for (int half = 0; half < 2; half++) {
+            __syncthreads();                       // acc writes (previous step) / sb readers done
             // d = acc X^e - acc of this half (thread-private slots of sd; branchless rotation)
             const u64* src = sacc + half * N;
 #pragma unroll
@@ -303,52 +327,59 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
               const u64 rv = (idx >= N && v) ? Q - v : v;
               sd[pos] = sub_mod(rv, src[pos], Q);
             }
-            const u64* sdh = sd;
+            // digit pairs (r, r+1) transformed together; an odd ell pairs the last digit with zero
 #pragma unroll 1
-            for (int r = 0; r < ell; r++) {
-              const u32* Kb = K + (size_t)((half * ell + r) * 2) * N;
-              const u32* Ka = Kb + N;
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb));
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(Ka));
-              u32 x[8];
+            for (int r = 0; r < ell; r += 2) {
+              const bool two = r + 1 < ell;
+              const u32* Kb0 = K + (size_t)((half * ell + r) * 2) * N;
+              const u32* Kb1 = Kb0 + 2 * N;
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb0));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb0 + N));
+              if (two) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1 + N));
+              }
+              u32 x[2][8];
               const int sh = r * logL;
 #pragma unroll
-              for (int k = 0; k < 8; k++) x[k] = (u32)(sdh[tid + T * k] >> sh) & dmask;
-              ntt_fwd32<N>(x, buf ? sb1 : sb0, tid, ft, pr, pr2);
-              buf ^= 1;
-              const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
-              const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
-              const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
-              const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
-#pragma unroll
               for (int k = 0; k < 8; k++) {
-                const u32 xr = csub32(csub32(x[k], pr2), pr);          // [0, p)
-                mb[k] += (u64)xr * kb[k];                              // < 2 ell p^2 < 2^63
-                ma[k] += (u64)xr * ka[k];
+                const u64 dv = sd[tid + T * k];
+                x[0][k] = (u32)(dv >> sh) & dmask;
+                x[1][k] = two ? (u32)(dv >> (sh + logL)) & dmask : 0u;
+              }
+              if (r > 0) __syncthreads();          // previous pair's readers of sb done
+              ntt_fwd32<N, 2>(x, sb, tid, ft, pr, pr2);
+#pragma unroll
+              for (int v = 0; v < 2; v++) {
+                if (v == 1 && !two) break;
+                const u32* Kb = v ? Kb1 : Kb0;
+                const u32* Ka = Kb + N;
+                const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
+                const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
+                const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
+                const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                  const u32 xr = csub32(csub32(x[v][k], pr2), pr);       // [0, p)
+                  mb[k] += (u64)xr * kb[k];                              // < 2 ell p^2 < 2^61
+                  ma[k] += (u64)xr * ka[k];
+                }
               }
             }
           }
-          // the a-column sums wait in the idle exchange buffer (buf ^ 1) during INTT(b): after
-          // the last forward transform's barrier each warp only touches its own 8T/W-element
-          // region of that buffer, and slots 8 tid + k lie in it
-          u32 xb[8];
-          u32* park = buf ? sb0 : sb1;
-          const int parkb = lay_base<N, S::NMID - 1>(8 * tid);     // the thread's PL slots
+          // both output columns through one paired inverse transform (warp-local start)
+          u32 x[2][8];
 #pragma unroll
-          for (int k = 0; k < 8; k++) { xb[k] = red64(mb[k], R, pi); park[parkb + k] = red64(ma[k], R, pi); }
-#pragma unroll 1
+          for (int k = 0; k < 8; k++) { x[0][k] = red64(mb[k], R, pi); x[1][k] = red64(ma[k], R, pi); }
+          ntt_inv32<N, 2>(x, sb, tid, it, pr, pr2);
+#pragma unroll
           for (int c = 0; c < 2; c++) {
-            u32 x[8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) x[k] = c ? park[parkb + k] : xb[k];
-            ntt_inv32<N>(x, buf ? sb1 : sb0, tid, it, pr, pr2);
-            buf ^= 1;
             u32* s0 = st0 + c * N;
             u32* s1 = st1 + c * N;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
               const int pos = tid + T * k;
-              const u32 rv = csub32(x[k], pr);                         // residue mod p_pi, [0, p)
+              const u32 rv = csub32(x[c][k], pr);                      // residue mod p_pi, [0, p)
               if (pi == 0) {
                 s0[pos] = rv;
               } else if (pi == 1) {
@@ -374,7 +405,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 const u32 c2 = csub32(csub32(u1 + R.p2[2] - u2, R.p2[2]), R.p[2]);  // [0, p2)
                 u64 v = shoup64_32(c0, R.m0, R.m0s, Q) + shoup64_32(c1, R.m1, R.m1s, Q) +
                         shoup64_32(c2, R.m2, R.m2s, Q);                                     // < 6Q
-                if (c2 > (R.p[2] >> 1)) v += Q - R.pmq;                             // V < 0
+                if (c2 > (R.p[2] >> 1)) v += Q - R.pmq;                                     // V < 0
                 v = csub(csub(v, Q << 2), Q << 1);
                 v = csub(v, Q);
                 sacc[c * N + pos] = add_mod(sacc[c * N + pos], v, Q);
@@ -409,14 +440,14 @@ k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, 
   const int r = (int)(frow % rows_per_step);
   const u32 pr = R.p[pi], pr2 = R.p2[pi];
   const u64* src = canon + poly * N;
-  u32 x[8];
+  u32 x[1][8];
 #pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = (u32)(src[tid + T * k] % pr);
-  ntt_fwd32<N>(x, sb, tid, R.ftab + (size_t)pi * S::GROUPS * 4, pr, pr2);
+  for (int k = 0; k < 8; k++) x[0][k] = (u32)(src[tid + T * k] % pr);
+  ntt_fwd32<N, 1>(x, sb, tid, R.ftab + (size_t)pi * S::GROUPS * 4, pr, pr2);
   u32* o = dev + ((step * R.np + pi) * rows_per_step + r) * 2 * (size_t)N + (size_t)col * N + 8 * tid;
 #pragma unroll
   for (int k = 0; k < 8; k++) {
-    const u32 v = csub32(csub32(x[k], pr2), pr);
+    const u32 v = csub32(csub32(x[0][k], pr2), pr);
     o[k] = csub32(shoup32(v, R.ninv[pi], R.ninvs[pi], pr), pr);
   }
 }
