@@ -56,6 +56,7 @@ struct RnsParams {
   u32 g01, g01s, g02, g02s, g12, g12s;
   u64 m0, m0s, m1, m1s, m2, m2s;          // 1, p0, p0 p1 mod Q (+ 64-bit Shoup companions)
   u64 pmq;                                // P mod Q (sign correction)
+  u32 zero;                               // 0, opaque to the compiler (see bfw32)
   const uint4* ftab;                      // [np][GROUPS][8 pairs] forward (w, w') u32
   const uint4* itab;                      // inverse
 };
@@ -66,20 +67,19 @@ FDFB_DEV u32 shoup32(u32 a, u32 w, u32 ws, u32 p) {     // a*w mod p in [0, 2p),
 }
 FDFB_DEV u32 csub32(u32 x, u32 m) { return min(x, x - m); }
 
-// Harvey butterflies with every add written as a 3-input IADD3 (keeps the adds on the ALU
-// pipe; two-input adds are otherwise issued as IMAD.IADD on the multiply pipe) and the
-// conditional subtractions as unsigned min (VIADDMNMX).  Needs 6p < 2^32 (p < 2^29).
-FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // CT, in/out [0, 4p)
+// Harvey butterflies.  ptxas issues two-input integer adds as IMAD.IADD on the (binding)
+// multiply pipe; every add here therefore carries a third, opaque zero operand z (a kernel
+// parameter the compiler cannot fold), which keeps it a 3-input IADD3 on the ALU pipe.
+// Conditional subtractions are unsigned min (VIADDMNMX).  Needs 6p < 2^32 (p < 2^29).
+FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // CT, [0, 4p)
   const u32 t = shoup32(Y, w, ws, p);                                   // [0, 2p)
-  const u32 s = X + t - p2;                                             // [-2p, 4p)
-  const u32 y = X - t + p2;                                             // (0, 6p)
-  X = min(s, s + p2);                                                   // [0, 4p)
-  Y = min(y, y - p2);                                                   // [0, 4p)
+  const u32 x = csub32(X, p2);                                          // [0, 2p)
+  X = x + t + z;                                                        // [0, 4p)
+  Y = x - t + p2;                                                       // (0, 4p)
 }
-FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2) {   // GS, in/out [0, 2p)
+FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // GS, [0, 2p)
   const u32 x = X, y = Y;
-  const u32 s = x + y - p2;                                             // [-2p, 2p)
-  X = min(s, s + p2);                                                   // [0, 2p)
+  X = csub32(x + y + z, p2);                                            // [0, 2p)
   Y = shoup32(x - y + p2, w, ws, p);                                    // [0, 2p)
 }
 
@@ -95,47 +95,47 @@ FDFB_DEV void load_tw8(Tw8& t, const uint4* g) {
 // V polynomials (V = 1 or 2) share every twiddle: twice the ILP and half the twiddle
 // loads per polynomial when two digit (or two column) transforms run together.
 template <int V>
-FDFB_DEV void fwd8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
+FDFB_DEV void fwd8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   Tw8 t; load_tw8(t, g);
 #pragma unroll
   for (int v = 0; v < V; v++) {
 #pragma unroll
-    for (int k = 0; k < 4; k++) bfw32(x[v][k], x[v][k + 4], t.w[0], t.s[0], p, p2);
+    for (int k = 0; k < 4; k++) bfw32(x[v][k], x[v][k + 4], t.w[0], t.s[0], p, p2, z);
   }
 #pragma unroll
   for (int v = 0; v < V; v++) {
-    bfw32(x[v][0], x[v][2], t.w[1], t.s[1], p, p2); bfw32(x[v][1], x[v][3], t.w[1], t.s[1], p, p2);
-    bfw32(x[v][4], x[v][6], t.w[2], t.s[2], p, p2); bfw32(x[v][5], x[v][7], t.w[2], t.s[2], p, p2);
+    bfw32(x[v][0], x[v][2], t.w[1], t.s[1], p, p2, z); bfw32(x[v][1], x[v][3], t.w[1], t.s[1], p, p2, z);
+    bfw32(x[v][4], x[v][6], t.w[2], t.s[2], p, p2, z); bfw32(x[v][5], x[v][7], t.w[2], t.s[2], p, p2, z);
   }
 #pragma unroll
   for (int v = 0; v < V; v++) {
 #pragma unroll
-    for (int k = 0; k < 4; k++) bfw32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
+    for (int k = 0; k < 4; k++) bfw32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2, z);
   }
 }
 template <int V>
-FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
+FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   Tw8 t; load_tw8(t, g);
 #pragma unroll
   for (int v = 0; v < V; v++) {
 #pragma unroll
-    for (int k = 0; k < 4; k++) bin32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2);
+    for (int k = 0; k < 4; k++) bin32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2, z);
   }
 #pragma unroll
   for (int v = 0; v < V; v++) {
-    bin32(x[v][0], x[v][2], t.w[1], t.s[1], p, p2); bin32(x[v][1], x[v][3], t.w[1], t.s[1], p, p2);
-    bin32(x[v][4], x[v][6], t.w[2], t.s[2], p, p2); bin32(x[v][5], x[v][7], t.w[2], t.s[2], p, p2);
+    bin32(x[v][0], x[v][2], t.w[1], t.s[1], p, p2, z); bin32(x[v][1], x[v][3], t.w[1], t.s[1], p, p2, z);
+    bin32(x[v][4], x[v][6], t.w[2], t.s[2], p, p2, z); bin32(x[v][5], x[v][7], t.w[2], t.s[2], p, p2, z);
   }
 #pragma unroll
   for (int v = 0; v < V; v++) {
 #pragma unroll
-    for (int k = 0; k < 4; k++) bin32(x[v][k], x[v][k + 4], t.w[0], t.s[0], p, p2);
+    for (int k = 0; k < 4; k++) bin32(x[v][k], x[v][k + 4], t.w[0], t.s[0], p, p2, z);
   }
 }
 // final pass on positions 8 tid + k: P stages with pair distance t = 2^{P-1-s}; stage s
 // uses 8 >> (P - s) consecutive pairs of the thread's group
 template <int P, int V>
-FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
+FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   Tw8 t; load_tw8(t, g);
   int o = 0;
 #pragma unroll
@@ -145,13 +145,13 @@ FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
     for (int v = 0; v < V; v++) {
 #pragma unroll
       for (int k = 0; k < 8; k++)
-        if ((k & d) == 0) bfw32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
+        if ((k & d) == 0) bfw32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2, z);
     }
     o += 8 >> (P - s);
   }
 }
 template <int P, int V>
-FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
+FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   Tw8 t; load_tw8(t, g);
   int o = 8 - (8 >> P);
 #pragma unroll
@@ -162,7 +162,7 @@ FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2) {
     for (int v = 0; v < V; v++) {
 #pragma unroll
       for (int k = 0; k < 8; k++)
-        if ((k & d) == 0) bin32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2);
+        if ((k & d) == 0) bin32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2, z);
     }
   }
 }
@@ -205,58 +205,58 @@ FDFB_DEV void xstore(const u32 (&x)[V][8], u32* sb, int base, int S) {
 }
 
 template <int N, int q, int V>
-FDFB_DEV void fwd_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+FDFB_DEV void fwd_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   if constexpr (q < BrShape<N>::NMID) {
     constexpr int T1 = N >> (3 * q + 3);
     const int B = qbase<N, q>(tid);
     xload<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
-    fwd8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
+    fwd8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2, z);
     __syncwarp();
     xstore<N, q, V>(x, sb, lay_base<N, q>(B), T1);
     __syncwarp();
-    fwd_mid<N, q + 1, V>(x, sb, tid, tab, p, p2);
+    fwd_mid<N, q + 1, V>(x, sb, tid, tab, p, p2, z);
   }
 }
 template <int N, int q, int V>
-FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   if constexpr (q >= 1) {
     constexpr int T1 = N >> (3 * q + 3);
     const int B = qbase<N, q>(tid);
     xload<N, q, V>(x, sb, lay_base<N, q>(B), T1);
-    inv8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2);
+    inv8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2, z);
     __syncwarp();
     xstore<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
     __syncwarp();
-    inv_mid<N, q - 1, V>(x, sb, tid, tab, p, p2);
+    inv_mid<N, q - 1, V>(x, sb, tid, tab, p, p2, z);
   }
 }
 
 // Forward NTT mod p of V polynomials. In: x[v][k] = coefficient tid + T k, [0, 4p).
 // Out: slot 8 tid + k, [0, 4p).  The caller guarantees that no thread still reads sb.
 template <int N, int V>
-FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   using S = BrShape<N>;
   constexpr int T = S::T, NM = S::NMID;
-  fwd8_32<V>(x, tab, p, p2);
+  fwd8_32<V>(x, tab, p, p2, z);
   xstore<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
   __syncthreads();
-  fwd_mid<N, 1, V>(x, sb, tid, tab, p, p2);
+  fwd_mid<N, 1, V>(x, sb, tid, tab, p, p2, z);
   xload<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
-  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2);
+  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
 }
 // Inverse NTT mod p (unscaled) of V polynomials. In: slot 8 tid + k, [0, 2p).  Out:
 // coefficient tid + T k, [0, 2p).  Starts warp-locally; ends after a CTA barrier.
 template <int N, int V>
-FDFB_DEV void ntt_inv32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2) {
+FDFB_DEV void ntt_inv32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   using S = BrShape<N>;
   constexpr int T = S::T, NM = S::NMID;
-  inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2);
+  inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
   xstore<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
   __syncwarp();
-  inv_mid<N, NM - 1, V>(x, sb, tid, tab, p, p2);
+  inv_mid<N, NM - 1, V>(x, sb, tid, tab, p, p2, z);
   __syncthreads();
   xload<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
-  inv8_32<V>(x, tab, p, p2);
+  inv8_32<V>(x, tab, p, p2, z);
 }
 
 // s < 2^63 -> s mod p in [0, 2p):  s1 2^32 + s0 = s1 (2^32 mod p) + s0
@@ -348,7 +348,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 x[1][k] = two ? (u32)(dv >> (sh + logL)) & dmask : 0u;
               }
               if (r > 0) __syncthreads();          // previous pair's readers of sb done
-              ntt_fwd32<N, 2>(x, sb, tid, ft, pr, pr2);
+              ntt_fwd32<N, 2>(x, sb, tid, ft, pr, pr2, R.zero);
 #pragma unroll
               for (int v = 0; v < 2; v++) {
                 if (v == 1 && !two) break;
@@ -371,7 +371,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           u32 x[2][8];
 #pragma unroll
           for (int k = 0; k < 8; k++) { x[0][k] = red64(mb[k], R, pi); x[1][k] = red64(ma[k], R, pi); }
-          ntt_inv32<N, 2>(x, sb, tid, it, pr, pr2);
+          ntt_inv32<N, 2>(x, sb, tid, it, pr, pr2, R.zero);
 #pragma unroll
           for (int c = 0; c < 2; c++) {
             u32* s0 = st0 + c * N;
@@ -443,7 +443,7 @@ k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, 
   u32 x[1][8];
 #pragma unroll
   for (int k = 0; k < 8; k++) x[0][k] = (u32)(src[tid + T * k] % pr);
-  ntt_fwd32<N, 1>(x, sb, tid, R.ftab + (size_t)pi * S::GROUPS * 4, pr, pr2);
+  ntt_fwd32<N, 1>(x, sb, tid, R.ftab + (size_t)pi * S::GROUPS * 4, pr, pr2, R.zero);
   u32* o = dev + ((step * R.np + pi) * rows_per_step + r) * 2 * (size_t)N + (size_t)col * N + 8 * tid;
 #pragma unroll
   for (int k = 0; k < 8; k++) {
