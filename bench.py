@@ -37,17 +37,22 @@ IMAD_PER_MODMUL = 16
 
 
 def parse():
+    """CLI; --workload shift times fdfb_shift on the Shift/VectorPack configuration."""
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fdfb", choices=["fdfb", "reference"])
-    ap.add_argument("--config", default="large")
+    ap.add_argument("--config", default=None, help="configs/<name>.json (default: large / shift)")
+    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "shift"])
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="end-to-end steps (default: --steps)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.config is None:
+        a.config = "shift" if a.workload == "shift" else "large"
+    return a
 
 
 def algorithmic_work(cfg):
@@ -171,6 +176,181 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------- GPU arm
+class BootstrapWorkload:
+    """fdfb_bootstrap_batch over B LWE ciphertexts of the Large configuration."""
+    metric = "functional bootstraps/sec (N=2048)"
+    unit = "bootstraps/s"
+    kclass = "blind_rotate"
+    kernel = "k_blind_rotate<2048,3>"
+
+    def __init__(self, ctx, cfg, B, rank, world, dev, stream):
+        import torch
+        import synth
+        from paper_2109_02731_b200.dist import broadcast_keys, shard_range
+        self.ctx, self.cfg, self.B, self.stream = ctx, cfg, B, stream
+        t0 = time.perf_counter()
+        if rank == 0:
+            keys = ctx.keygen(cfg["seeds"]["keys"], which=0x0F)
+        else:
+            keys = {"s": torch.empty(ctx.n, dtype=torch.int8, device=dev),
+                    "S": torch.empty(ctx.N, dtype=torch.int8, device=dev),
+                    "brk": ctx._bytes(ctx.sizes["brk"]), "bpk": ctx._bytes(ctx.sizes["bpk"]),
+                    "ksk": ctx._bytes(ctx.sizes["ksk"]), "pack": None}
+        torch.cuda.synchronize()
+        self.keygen_s = time.perf_counter() - t0
+        self.bcast_s = 0.0
+        if world > 1:                           # one NCCL broadcast of every key over NVLink
+            t0 = time.perf_counter()
+            broadcast_keys(keys)
+            torch.cuda.synchronize()
+            self.bcast_s = time.perf_counter() - t0
+        self.keys = keys
+        self.f = synth.lut(cfg)
+        self.rotp = ctx.setup_lut(self.f)
+        start, count = shard_range(B * world, world, rank)
+        self.msgs = synth.messages(cfg, B * world)[start:start + count]
+        self.ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"] + rank, keys["s"],
+                                     torch.from_numpy(self.msgs.copy()).to(dev))
+        self.ct_out = torch.empty_like(self.ct_in)
+        self.ws = ctx.workspace_bootstrap(B)
+        self.io_bytes = B * (ctx.n + 1) * 8
+        self.key_bytes = ctx.sizes["brk"] + ctx.sizes["bpk"] + ctx.sizes["ksk"]
+
+    def step(self):
+        self.ctx.bootstrap_batch(self.keys, self.rotp, self.ct_in, self.ct_out, self.ws, stream=self.stream)
+
+    def host_buffers(self):
+        import torch
+        h_in = torch.empty(tuple(self.ct_in.shape), dtype=torch.uint64, pin_memory=True)
+        h_in.copy_(self.ct_in.cpu())
+        return h_in, torch.empty_like(h_in).pin_memory()
+
+    def step_host(self, h_in, h_out):
+        self.ctx.bootstrap_batch_host(self.keys, self.rotp, h_in, h_out, self.ws, stream=self.stream)
+
+    def spot_check(self):
+        """Decrypt 64 outputs with s (plain phase; no oracle) and count f(m) hits."""
+        import numpy as np
+        cfg = self.cfg
+        s_h = self.keys["s"].cpu().numpy().astype(np.int64).astype(np.uint64)
+        out_h = self.ct_out[:64].cpu().numpy()
+        q = 1 << cfg["log_q_lwe"]
+        ph = (out_h[:, 0] - (out_h[:, 1:] * s_h[None, :]).sum(axis=1)) & np.uint64(q - 1)
+        dec = ((ph.astype(object) * cfg["t"] * 2 + q) // (2 * q)) % cfg["t"]
+        ok = sum(int(a) == int(b) for a, b in zip(dec, self.f[self.msgs[:64]]))
+        return {"lut_spot_check": "%d/64 outputs decrypt to f(m)" % ok}
+
+    def roofline(self, kernel_ms_per_step, ms_step):
+        per_cmux, cmux_per_bs = algorithmic_work(self.cfg)
+        modmul_step = per_cmux * cmux_per_bs * self.B
+        imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
+        peak = 148 * IMAD_PER_SM_CLK * 1965e6
+        return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
+                "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None,
+                "modmul_per_step": modmul_step, "imad_per_modmul": IMAD_PER_MODMUL,
+                "modmul_per_s": modmul_step / (kernel_ms_per_step / 1e3),
+                "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; "
+                              "16 slots per 54-bit Shoup modmul"}
+
+    def config(self):
+        cfg = self.cfg
+        return {"workload": cfg["name"], "N": cfg["N"], "n": cfg["n"], "Q_bits": cfg["Q"].bit_length(),
+                "ell_boot": cfg["ell_boot"]}
+
+
+class ShiftWorkload:
+    """fdfb_shift over B RLWE ciphertexts of the Shift/VectorPack configuration
+    (N=2048, L_pK=2, ell_pK=54), d ~ U[1, N-1] per ciphertext."""
+    metric = "shifts/sec (N=2048, L_pK=2, ell_pK=54)"
+    unit = "shifts/s"
+    kclass = "shift"
+    kernel = "k_shift<8,4,true>"
+
+    def __init__(self, ctx, cfg, B, rank, world, dev, stream):
+        import torch
+        import synth
+        from paper_2109_02731_b200.dist import broadcast_keys, shard_range
+        self.ctx, self.cfg, self.B, self.stream = ctx, cfg, B, stream
+        t0 = time.perf_counter()
+        if rank == 0:
+            keys = ctx.keygen(cfg["seeds"]["keys"], which=0x11)
+        else:
+            keys = {"s": torch.empty(ctx.n, dtype=torch.int8, device=dev),
+                    "S": torch.empty(ctx.N, dtype=torch.int8, device=dev), "pack": ctx._bytes(ctx.sizes["pack"])}
+        torch.cuda.synchronize()
+        self.keygen_s = time.perf_counter() - t0
+        self.bcast_s = 0.0
+        if world > 1:
+            t0 = time.perf_counter()
+            broadcast_keys(keys)
+            torch.cuda.synchronize()
+            self.bcast_s = time.perf_counter() - t0
+        self.keys = keys
+        start, count = shard_range(B * world, world, rank)
+        self.msg = synth.rlwe_messages(cfg, B * world)[start:start + count]
+        self.d = synth.shift_amounts(cfg, B * world)[start:start + count]
+        self.ct_in = ctx.rlwe_encrypt(cfg["seeds"]["err"] + rank, keys["S"], torch.from_numpy(self.msg).to(dev))
+        self.d_dev = torch.from_numpy(self.d.astype("uint32")).to(dev)
+        self.ct_out = torch.empty_like(self.ct_in)
+        self.io_bytes = B * 2 * ctx.N * 8
+        self.key_bytes = ctx.sizes["pack"]
+
+    def step(self):
+        self.ctx.shift(self.keys["pack"], self.ct_in, self.d_dev, self.ct_out, stream=self.stream)
+
+    def host_buffers(self):
+        import torch
+        h_in = torch.empty(tuple(self.ct_in.shape), dtype=torch.uint64, pin_memory=True)
+        h_in.copy_(self.ct_in.cpu())
+        return h_in, torch.empty_like(h_in).pin_memory()
+
+    def step_host(self, h_in, h_out):
+        # host-buffer end to end through the public API: H2D, shift, D2H on the stream
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.ct_in.copy_(h_in, non_blocking=True)
+            self.step()
+            h_out.copy_(self.ct_out, non_blocking=True)
+        self.stream.synchronize()
+
+    def spot_check(self):
+        """Phase of 4 outputs (b - a*S, negacyclic, S ternary; numpy) equals roll(m, d) up to noise."""
+        import numpy as np
+        Q, N = self.cfg["Q"], self.cfg["N"]
+        Qu = np.uint64(Q)
+        S = self.keys["S"].cpu().numpy().astype(np.int64)
+        out = self.ct_out[:4].cpu().numpy()
+        worst = 0
+        for c in range(4):
+            ph = out[c, 0].copy()
+            a = out[c, 1]
+            for i in np.nonzero(S)[0]:          # subtract S_i X^i a (X^N = -1)
+                r = np.concatenate([(Qu - a[N - i:]) % Qu, a[:N - i]]) if i else a.copy()
+                if S[i] < 0:
+                    r = (Qu - r) % Qu
+                ph = np.where(ph >= r, ph - r, ph + Qu - r)
+            e = (ph.astype(object) - np.roll(self.msg[c], int(self.d[c])).astype(object)) % Q
+            worst = max(worst, max(min(int(x), Q - int(x)) for x in e))
+        return {"shift_spot_check": "max |phase - roll(m, d)| over 4 outputs = 2^%.1f (Q = 2^%.1f)"
+                                    % (np.log2(max(worst, 1)), np.log2(Q))}
+
+    def roofline(self, kernel_ms_per_step, ms_step):
+        # HBM roofline: the Delta table must be read at least once per batch (it is shared by
+        # every ciphertext), plus T1, U and the ciphertexts in and out.
+        lay_delta = self.cfg["ell_pack"] * (self.cfg["N"] - 1) * (2 * self.cfg["N"]) * 8
+        algo = lay_delta + 2 * self.io_bytes
+        gbs = algo / (kernel_ms_per_step / 1e3) / 1e9
+        peak = json.load(open(PEAKS_FILE))["hbm_gbs"] if os.path.exists(PEAKS_FILE) else 6650.0
+        return {"kernel": self.kernel, "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                "frac": gbs / peak, "traffic": None, "algorithmic_bytes_per_step": algo,
+                "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if os.path.exists(PEAKS_FILE) else "fallback 6.65 TB/s"}
+
+    def config(self):
+        cfg = self.cfg
+        return {"workload": cfg["name"], "N": cfg["N"], "ell_pack": cfg["ell_pack"], "L_pack": 1 << cfg["logL_pack"],
+                "d": "U[1, N-1] per ciphertext"}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -180,12 +360,12 @@ def main():
         run_reference(args, rank, world)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import synth
     from paper_2109_02731_b200 import Context
+    from paper_2109_02731_b200.dist import max_over_ranks
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -195,53 +375,19 @@ def main():
     B = args.batch or cfg["batch"]
     ctx = Context(cfg, local)
     stream = torch.cuda.current_stream()
-
-    # keys: generated once (rank 0), broadcast over NVLink (NCCL) -- outside the timed region
-    t0 = time.perf_counter()
-    keys = ctx.keygen(cfg["seeds"]["keys"], which=0x0F) if rank == 0 or world == 1 else {
-        "s": torch.empty(ctx.n, dtype=torch.int8, device=dev), "S": torch.empty(ctx.N, dtype=torch.int8, device=dev),
-        "brk": ctx._bytes(ctx.sizes["brk"]), "bpk": ctx._bytes(ctx.sizes["bpk"]), "ksk": ctx._bytes(ctx.sizes["ksk"])}
-    torch.cuda.synchronize()
-    keygen_s = time.perf_counter() - t0
-    bcast_s = 0.0
-    if world > 1:
-        t0 = time.perf_counter()
-        for k in ("s", "S", "brk", "bpk", "ksk"):
-            dist.broadcast(keys[k], src=0)
-        torch.cuda.synchronize()
-        bcast_s = time.perf_counter() - t0
-
-    # inputs: this rank's contiguous shard of the seeded batch, encrypted on the device
-    f = synth.lut(cfg)
-    rotp = ctx.setup_lut(f)
-    msgs_all = synth.messages(cfg, B * world)
-    msgs = torch.from_numpy(msgs_all[rank * B:(rank + 1) * B].copy()).to(dev)
-    ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"] + rank, keys["s"], msgs)
-    ct_out = torch.empty_like(ct_in)
-    ws = ctx.workspace_bootstrap(B)
+    W = (ShiftWorkload if args.workload == "shift" else BootstrapWorkload)(ctx, cfg, B, rank, world, dev, stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MB > 126 MB L2
     torch.cuda.synchronize()
 
-    def step():
-        ctx.bootstrap_batch(keys, rotp, ct_in, ct_out, ws, stream=stream)
-
     for _ in range(args.warmup):
         flush.zero_()
-        step()
+        W.step()
     torch.cuda.synchronize()
-
-    # correctness spot check (not timed): decrypt a few outputs with s (plain phase, no oracle)
-    s_h = keys["s"].cpu().numpy().astype(np.int64).astype(np.uint64)
-    out_h = ct_out[:64].cpu().numpy()
-    q = 1 << cfg["log_q_lwe"]
-    ph = (out_h[:, 0] - (out_h[:, 1:] * s_h[None, :]).sum(axis=1)) & np.uint64(q - 1)
-    dec = ((ph.astype(object) * cfg["t"] * 2 + q) // (2 * q)) % cfg["t"]
-    want = f[msgs_all[rank * B:rank * B + 64]]
-    lut_ok = int(sum(int(a) == int(b) for a, b in zip(dec, want)))
+    extra = W.spot_check() if rank == 0 else {}
 
     # ------------------------------------------------------------------ timed region
     ctx.timing_enable(True)
-    ctx.timing_read("blind_rotate")
+    ctx.timing_read(W.kclass)
     launches0 = ctx.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
@@ -252,7 +398,7 @@ def main():
     for i in range(args.steps):
         flush.zero_()                          # L2 flush between timed steps (outside the events)
         evs[i][0].record(stream)
-        step()
+        W.step()
         evs[i][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -260,21 +406,17 @@ def main():
     clocks = clk.stop()
     launches = ctx.launch_count() - launches0
     ms = sum(a.elapsed_time(b) for a, b in evs)
-    br_ms, br_launches = ctx.timing_read("blind_rotate")
+    k_ms, k_launches = ctx.timing_read(W.kclass)
     ctx.timing_enable(False)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, device=dev)
     ms_step = ms / args.steps
     value = B * world / (ms_step / 1e3)
 
     # ------------------------------------------------------------------ end to end (host buffers)
     e2e_steps = args.e2e_steps or args.steps
-    h_in = torch.empty((B, ctx.n + 1), dtype=torch.uint64, pin_memory=True)
-    h_in.copy_(ct_in.cpu())
-    h_out = torch.empty_like(h_in).pin_memory()
-    ctx.bootstrap_batch_host(keys, rotp, h_in, h_out, ws, stream=stream)   # warm
+    h_in, h_out = W.host_buffers()
+    W.step_host(h_in, h_out)                   # warm
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -284,50 +426,36 @@ def main():
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        ctx.bootstrap_batch_host(keys, rotp, h_in, h_out, ws, stream=stream)
+        W.step_host(h_in, h_out)
         b.record(stream)
         b.synchronize()
         e_ms += a.elapsed_time(b)
     if world > 1:
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
+        e_ms = max_over_ranks(e_ms, device=dev)
     e2e_value = B * world / (e_ms / e2e_steps / 1e3)
-    e2e_ok = bool(torch.equal(h_out, ct_out.cpu()))
+    e2e_ok = bool(torch.equal(h_out, W.ct_out.cpu()))
 
     if rank == 0:
-        per_cmux, cmux_per_bs = algorithmic_work(cfg)
-        n_acc = B * (cfg["ell_boot"] + 1)
-        br_launch_ms = br_ms / max(1, br_launches)
-        # one step launches BR twice: B*ell_boot accumulators, then B; algorithmic modmul per step
-        modmul_step = per_cmux * cmux_per_bs * B
-        imad_s = modmul_step * IMAD_PER_MODMUL / (br_ms / args.steps / 1e3)
-        peak = 148 * IMAD_PER_SM_CLK * 1965e6
+        kms_step = k_ms / args.steps
+        roof = W.roofline(kms_step, ms_step)
+        roof.update({"kernel_ms_per_step": kms_step, "kernel_launches": k_launches,
+                     "kernel_share_of_step": kms_step / ms_step})
+        cfgd = W.config()
+        cfgd.update({"per_gpu_batch": B, "global_batch": B * world, "parallelism": "dp%d" % world,
+                     "l2": "flushed between timed steps (256 MB write)", "keys_resident_bytes": W.key_bytes})
         line = {
-            "metric": "functional bootstraps/sec (N=2048)", "value": value, "unit": "bootstraps/s",
+            "metric": W.metric, "value": value, "unit": W.unit,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic",
-            "config": {"workload": cfg["name"], "N": cfg["N"], "n": cfg["n"], "Q_bits": cfg["Q"].bit_length(),
-                       "per_gpu_batch": B, "global_batch": B * world, "ell_boot": cfg["ell_boot"],
-                       "parallelism": "dp%d" % world, "l2": "flushed between timed steps (256 MB write)",
-                       "keys_resident_bytes": ctx.sizes["brk"] + ctx.sizes["bpk"] + ctx.sizes["ksk"]},
-            "gpu_launches": launches,
-            "e2e": {"value": e2e_value, "unit": "bootstraps/s", "steps": e2e_steps,
-                    "h2d_bytes_per_step": B * (ctx.n + 1) * 8, "d2h_bytes_per_step": B * (ctx.n + 1) * 8,
+            "data": "synthetic", "config": cfgd, "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": W.unit, "steps": e2e_steps,
+                    "h2d_bytes_per_step": W.io_bytes, "d2h_bytes_per_step": W.io_bytes,
                     "matches_device_path": e2e_ok},
-            "roofline": {"kernel": "k_blind_rotate<2048>", "bound": "alu", "achieved": imad_s / 1e12,
-                         "peak": peak / 1e12, "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None,
-                         "modmul_per_step": modmul_step, "imad_per_modmul": IMAD_PER_MODMUL,
-                         "br_ms_per_step": br_ms / args.steps, "br_launches": br_launches,
-                         "br_ms_per_launch": br_launch_ms, "br_share_of_step": (br_ms / args.steps) / ms_step,
-                         "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; 16 slots per 54-bit Shoup modmul",
-                         "modmul_per_s": modmul_step / (br_ms / args.steps / 1e3)},
-            "clocks": clocks,
-            "lut_spot_check": "%d/64 outputs decrypt to f(m)" % lut_ok,
-            "keygen_s": keygen_s, "key_broadcast_s": bcast_s,
+            "roofline": roof, "clocks": clocks,
+            "keygen_s": W.keygen_s, "key_broadcast_s": W.bcast_s,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        line.update(extra)
+        if world == 1 and not args.no_cpu_baseline and args.workload == "bootstrap":
             cb = cpu_oracle_sample(cfg, args.cpu_seconds)
             cb.pop("seconds", None)
             line["cpu_baseline"] = cb
