@@ -284,3 +284,38 @@ def test_shift_out_of_range_d_flagged():
         ctx.device_status()
     assert not got[0].any() and not got[2].any()
     ctx.device_status()                                          # cleared
+
+
+# ----------------------------------------------------------------------------- full-size (bench launch configuration)
+@pytest.mark.slow
+def test_bootstrap_large_full_batch_sampled_bit_exact():
+    """Large configuration at the bench's batch (B = 4096 -> one blind-rotation launch over
+    28672 accumulators, then 4096): two sampled outputs bit-exact with the oracle, which
+    computes them one at a time (schoolbook, ~2 min each on the host cores)."""
+    cfg, orc, K, ctx, dk = setup("large")
+    f = synth.lut(cfg)
+    rotp = orc.setup_polynomial(orc.bootsmap(f))
+    B = cfg["batch"]
+    msgs = synth.messages(cfg, B)
+    cts = orc.lwe_encrypt(cfg["seeds"]["err"], K["s"], msgs)
+    got = H(ctx.bootstrap_batch(dk, ctx.setup_lut(f), T(cts)))
+    for i in (0, B - 1):
+        assert np.array_equal(got[i], orc.bootstrap(K, rotp, cts[i:i + 1])[0]), i
+
+
+def test_bootstrap_large_full_batch_noiseless_full_domain():
+    """Property at full size: noiseless keys and mod-switch-exact inputs -> every one of the
+    4096 outputs decrypts exactly to f(m) (Thm), all 256 messages."""
+    cfg = synth.load_config("large")
+    ctx = Context(cfg, 0, noiseless=True)
+    keys = ctx.keygen(cfg["seeds"]["keys"])
+    f = synth.lut(cfg, seed=77)
+    B = cfg["batch"]
+    msgs = np.arange(B, dtype=np.uint64) % cfg["t"]
+    cts = ctx.lwe_encrypt(5, keys["s"], T(msgs), exact=True)
+    out = H(ctx.bootstrap_batch(keys, ctx.setup_lut(f), cts))
+    s = H(keys["s"]).astype(np.int64).astype(np.uint64)
+    q = 1 << cfg["log_q_lwe"]
+    ph = (out[:, 0] - (out[:, 1:] * s[None, :]).sum(axis=1)) & np.uint64(q - 1)
+    dec = ((ph.astype(object) * cfg["t"] * 2 + q) // (2 * q)) % cfg["t"]
+    assert [int(x) for x in dec] == [int(f[int(m)]) for m in msgs]
