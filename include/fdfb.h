@@ -165,10 +165,17 @@ int fdfb_pack(const fdfb_ctx* ctx, const void* pack, const uint64_t* lwe, const 
               uint32_t B, void* stream);
 /* Shift (readings F2/F3/G4): rlwe_in [dev, B x 2N] mod Q encrypting m,
  * d [dev, B, 1..N-1] -> rlwe_out [dev, B x 2N] encrypting the cyclic rotation of m by d.
- * Computed through the exact suffix-sum form of VectorPack.  A d outside
- * 1..N-1 yields a zero row and raises the fdfb_device_status flag.  workspace may be NULL. */
+ * VectorPack is evaluated through the exact suffix-sum identity of DESIGN.md; for
+ * L_pack = 2 as one int8 tensor-core GEMM (bit matrix x balanced base-256 key digits,
+ * exact in int32) plus a finishing kernel -- workspace [dev] of fdfb_workspace_shift(ctx, B)
+ * bytes is then required (FDFB_E_WORKSPACE if NULL); for L_pack > 2 by the streaming kernel
+ * (workspace may be NULL).  A d outside 1..N-1 yields a zero row and raises the
+ * fdfb_device_status flag. */
 int fdfb_shift(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* d,
                uint64_t* rlwe_out, uint32_t B, void* workspace, void* stream);
+/* The same Shift through the streaming (CUDA-core) kernel for any L_pack; no workspace. */
+int fdfb_shift_streaming(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* d,
+                         uint64_t* rlwe_out, uint32_t B, void* stream);
 
 /* ------------------------------------------------------------------ kernel unit tests
  * Negacyclic ring product through the NTT kernels: c = a * b mod (X^N+1, Q),
@@ -182,7 +189,7 @@ int fdfb_cdt_table(const fdfb_ctx* ctx, uint64_t* thr, int* T);
  * fdfb_timing_read waits for the recorded events of class `kclass`, returns their
  * summed device time (ms) and launch count, and forgets them. */
 enum { FDFB_KCLASS_BLIND_ROTATE = 0, FDFB_KCLASS_KEYSWITCH_RLWE = 1, FDFB_KCLASS_KEYSWITCH_LWE = 2,
-       FDFB_KCLASS_SHIFT = 3 };
+       FDFB_KCLASS_SHIFT = 3, FDFB_KCLASS_SHIFT_GEMM = 4 };
 int fdfb_timing_enable(const fdfb_ctx* ctx, int on);
 int fdfb_timing_read(const fdfb_ctx* ctx, int kclass, double* total_ms, uint64_t* launches);
 /* Device-side argument errors of earlier stream-ordered calls: synchronises, returns

@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cublasLt.h>
+
 #include "../../include/fdfb.h"
 #include "kernels_boot.cuh"
 #include "kernels_shift.cuh"
@@ -33,6 +35,8 @@ struct fdfb_ctx {
   mutable std::mutex tmu;
   mutable bool timing = false;
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
+  mutable std::mutex lt_mu;
+  mutable cublasLtHandle_t lt = nullptr;   // Shift-as-GEMM (int8 tensor-core GEMM, created lazily)
 };
 
 // Bracket one launch of kernel class `cls` with events on its stream when timing is on.
@@ -402,6 +406,7 @@ extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
   cudaFree(c->d_rtab);
+  if (c->lt) cublasLtDestroy(c->lt);
   delete c;
 }
 

@@ -7,6 +7,8 @@
 //   D   Delta^{(v)}_{i,j}, i = 2..N, v>=1 [ell][N-1][L-1][2][N]
 //   U   sum_j sum_{i>=2} T^{(0)}_{i,j}   [2][N]
 //   Uj  per-j partials of U              [ell][2][N]
+//   S0  sum_j T^{(0)}_{1,j}              [2][N]        (L == 2: Shift-as-GEMM key below)
+//   GK  int8 [7 * 2N][Kpad] balanced base-256 digits of the GEMM key matrix
 // with the key-only suffix sums  T^{(v)}_{i,j} = sum_{i'>=i} X^{i'-i} pK[i',j,v]  and
 // Delta^{(v)}_{i,j} = T^{(v)}_{i,j} - T^{(0)}_{i,j}.
 //
@@ -24,8 +26,14 @@
 struct PackLayout {
   size_t P;                 // words per RLWE (2N)
   size_t A, T1, D, U, Uj;   // word offsets
+  size_t S0, GK;            // L == 2 only: S0 = sum_j T^(0)_{1,j} [2][N]; GEMM key digits (int8, see below)
   size_t words;
 };
+static inline size_t shift_gemm_key_bytes(int N, int ell, int L) {
+  if (L != 2) return 0;
+  const size_t K = (size_t)ell * (N - 1) + N + (size_t)ell * N, Kpad = (K + 15) & ~(size_t)15;
+  return 7 * 2 * (size_t)N * Kpad;
+}
 static inline PackLayout pack_layout(int N, int ell, int L) {
   PackLayout l;
   l.P = 2 * (size_t)N;
@@ -34,7 +42,9 @@ static inline PackLayout pack_layout(int N, int ell, int L) {
   l.D = l.T1 + (size_t)ell * L * l.P;
   l.U = l.D + (size_t)ell * (N - 1) * (L - 1) * l.P;
   l.Uj = l.U + l.P;
-  l.words = l.Uj + (size_t)ell * l.P;
+  l.S0 = l.Uj + (size_t)ell * l.P;
+  l.GK = l.S0 + l.P;
+  l.words = l.GK + (shift_gemm_key_bytes(N, ell, L) + 7) / 8;
   return l;
 }
 
@@ -319,4 +329,174 @@ k_vector_pack(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64
   }
 #pragma unroll
   for (int r = 0; r < CPT; r++) out[(size_t)b * 2 * N + (size_t)h * N + tid + r * TPB] = acc[r];
+}
+
+// ===========================================================================
+// Shift as one exact int8 GEMM (L_pack == 2).
+// With A_k[i,j] = bit_j(a'_k[i]) the packed sum of Shift's VectorPack is, per ciphertext,
+//   G  = sum_{j,i'} gamma_{i',j} Delta_{i'+1,j} + sum_{k<m} X^k S0 + sum_{j,k<m} A_{k+1}[1,j] X^k Delta_{1,j}
+//   Bs = sum_{j,i'} beta_{i',j}  Delta_{i'+1,j}
+// (S0 = sum_j T^(0)_{1,j}), i.e. a 0/1 matrix (rows: G and Bs of every ciphertext; columns:
+// the GK = ell(N-1) + N + ell N "terms") times the key matrix whose row for each term is
+// the term polynomial pair.  Key coefficients (< 2^54) are split into 7 balanced base-256
+// digits, so the product is 7 int8 GEMMs done as one (N_out = 7 * 2N), exact in int32
+// (|sum| <= GK * 128 < 2^31); k_shift_gemm_finish recombines the digits mod Q.
+struct ShiftGemm {
+  int K;        // number of terms ell(N-1) + N + ell N
+  int Kpad;     // K rounded up to a multiple of 16
+  int Nout;     // 7 * 2N
+};
+static inline ShiftGemm shift_gemm_shape(int N, int ell) {
+  ShiftGemm s;
+  s.K = ell * (N - 1) + N + ell * N;
+  s.Kpad = (s.K + 15) & ~15;
+  s.Nout = 7 * 2 * N;
+  return s;
+}
+// term kk, coefficient w (of the 2N-word pair) of the key matrix
+FDFB_DEV u64 shift_term(const DevParams& p, const u64* __restrict__ pk, const PackLayout& lay, const u64* __restrict__ S0,
+                        int kk, int w) {
+  const int N = p.N, ell = p.ell_pack;
+  const int h = w / N, x = w % N;
+  const int s1 = ell * (N - 1);
+  if (kk < s1) {                                  // Delta_{i'+1, j}, j = kk / (N-1), i'+1 = kk % (N-1) + 2
+    const int j = kk / (N - 1), t = kk % (N - 1);
+    return pk[lay.D + ((size_t)j * (N - 1) + t) * lay.P + w];
+  }
+  kk -= s1;
+  const u64* src;
+  int k;
+  if (kk < N) { src = S0 + (size_t)h * N; k = kk; }                         // X^k S0
+  else {                                                                    // X^k Delta_{1,j}
+    kk -= N;
+    const int j = kk / N;
+    k = kk % N;
+    src = pk + lay.T1 + ((size_t)j * 2 + 1) * lay.P + (size_t)h * N;       // T^(1)_{1,j} ...
+    const u64* t0 = pk + lay.T1 + ((size_t)j * 2) * lay.P + (size_t)h * N;  // ... minus T^(0)_{1,j}
+    const int e = x - k;
+    const int ix = e >= 0 ? e : e + N;
+    const u64 v = sub_mod(src[ix], t0[ix], p.Q);
+    return e >= 0 ? v : neg_mod(v, p.Q);
+  }
+  const int e = x - k;
+  return e >= 0 ? src[e] : neg_mod(src[e + N], p.Q);
+}
+// S0[h][x] = sum_j T^(0)_{1,j}
+__global__ void k_shift_s0(DevParams p, const u64* __restrict__ pk, PackLayout lay, u64* __restrict__ S0) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= 2 * p.N) return;
+  u64 s = 0;
+  for (int j = 0; j < p.ell_pack; j++) s = add_mod(s, pk[lay.T1 + ((size_t)j * 2) * lay.P + w], p.Q);
+  S0[w] = s;
+}
+// GK[l * 2N + w][kk] = balanced digit l of term kk at coefficient w.  Tile: 32 terms x 8 coefficients.
+__global__ void k_shift_gemm_key(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ S0,
+                                 ShiftGemm g, int8_t* __restrict__ GK) {
+  const int kk = blockIdx.x * 32 + threadIdx.x;
+  const int w = blockIdx.y * 8 + threadIdx.y;
+  if (w >= 2 * p.N) return;
+  u64 v = 0;
+  if (kk < g.K) v = shift_term(p, pk, lay, S0, kk, w);
+  if (kk >= g.Kpad) return;
+#pragma unroll
+  for (int l = 0; l < 7; l++) {
+    int t = (int)(v & 255);
+    if (t >= 128) t -= 256;
+    v = (u64)((long long)v - t) >> 8;
+    GK[((size_t)l * 2 * p.N + w) * g.Kpad + kk] = (int8_t)t;
+  }
+}
+// Per-batch 0/1 matrix: rows 2c (G) and 2c+1 (Bs) of ciphertext c.
+__global__ void k_shift_bits(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ dd, int B, ShiftGemm g,
+                             int8_t* __restrict__ A, int* __restrict__ status) {
+  const int c = blockIdx.y;
+  const int N = p.N, ell = p.ell_pack;
+  int d = (int)dd[c];
+  const bool ok = d >= 1 && d <= N - 1;
+  if (!ok) { if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, 1); d = 1; }
+  const bool br1 = 2 * d <= N;
+  const int m = br1 ? d : N - d, K1 = br1 ? N - d + 1 : 1, Km = K1 + m - 1;
+  const u64* a = ct + (size_t)c * 2 * N + N;
+  int8_t* rg = A + (size_t)(2 * c) * g.Kpad;
+  int8_t* rb = rg + g.Kpad;
+  const int s1 = ell * (N - 1);
+  for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < g.Kpad; kk += gridDim.x * blockDim.x) {
+    int8_t vg = 0, vb = 0;
+    if (ok && kk < s1) {
+      const int j = kk / (N - 1), t = kk % (N - 1);            // i' = t + 1
+      vg = (int8_t)((sx_mask(a, K1, t + 2, N, p.Q) >> j) & 1);
+      vb = (int8_t)((sx_mask(a, Km, t + 1, N, p.Q) >> j) & 1);
+    } else if (ok && kk < s1 + N) {
+      vg = (kk - s1) < m ? 1 : 0;
+    } else if (ok && kk < g.K) {
+      const int r = kk - s1 - N, j = r / N, k = r % N;
+      vg = k < m ? (int8_t)((a[K1 + k - 1] >> j) & 1) : 0;
+    }
+    rg[kk] = vg;
+    rb[kk] = vb;
+  }
+}
+// Recombine digits (int32 D[row][l * 2N + w]) mod Q and assemble Shift's output, one CTA
+// of 256 threads per (ciphertext, column):  S = G + U - X^m (U + Bs);  P = [bsum, 0] - S;
+// branch 1: out = ct X^d + 2P;  branch 2: out = (2P - ct) X^d.
+template <int CPT>
+__global__ void __launch_bounds__(256)
+k_shift_gemm_finish(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ ct,
+                    const u32* __restrict__ dd, const int* __restrict__ D, u64* __restrict__ out) {
+  constexpr int TPB = 256;
+  const int N = p.N, c = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const u64 Q = p.Q;
+  __shared__ u64 W[2048];
+  __shared__ u64 Pb[2048];
+  u64* o = out + (size_t)c * 2 * N + (size_t)h * N;
+  int d = (int)dd[c];
+  if (d < 1 || d > N - 1) {                     // flagged by k_shift_bits
+    for (int x = tid; x < N; x += TPB) o[x] = 0;
+    return;
+  }
+  const bool br1 = 2 * d <= N;
+  const int m = br1 ? d : N - d, K1 = br1 ? N - d + 1 : 1;
+  const int Nout = 7 * 2 * N;
+  const int* dg = D + (size_t)(2 * c) * Nout + (size_t)h * N;
+  const int* db = dg + Nout;
+  const u64* U = pk + lay.U + (size_t)h * N;
+  u64 G[CPT];
+#pragma unroll
+  for (int r = 0; r < CPT; r++) {
+    const int x = tid + r * TPB;
+    __int128 vg = 0, vb = 0;
+#pragma unroll
+    for (int l = 6; l >= 0; l--) {
+      vg = vg * 256 + dg[(size_t)l * 2 * N + x];
+      vb = vb * 256 + db[(size_t)l * 2 * N + x];
+    }
+    long long rg = (long long)(vg % (__int128)Q), rb = (long long)(vb % (__int128)Q);
+    G[r] = (u64)(rg < 0 ? rg + (long long)Q : rg);
+    const u64 bs = (u64)(rb < 0 ? rb + (long long)Q : rb);
+    W[x] = add_mod(__ldg(U + x), bs, Q);
+  }
+  __syncthreads();
+  const u64* cth = ct + (size_t)c * 2 * N + (size_t)h * N;
+#pragma unroll
+  for (int r = 0; r < CPT; r++) {
+    const int x = tid + r * TPB;
+    const int e = x - m;
+    const u64 rw = e >= 0 ? W[e] : neg_mod(W[e + N], Q);
+    const u64 S = sub_mod(add_mod(G[r], __ldg(U + x), Q), rw, Q);
+    u64 bs = 0;
+    if (h == 0 && x < m) bs = __ldg(ct + (size_t)c * 2 * N + (K1 + x - 1));
+    Pb[x] = sub_mod(bs, S, Q);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < CPT; r++) {
+    const int x = tid + r * TPB;
+    const u64 cr = rot_coeff(cth, x, d, N, Q);
+    if (br1) {
+      o[x] = add_mod(cr, add_mod(Pb[x], Pb[x], Q), Q);
+    } else {
+      const u64 pr = rot_coeff(Pb, x, d, N, Q);
+      o[x] = sub_mod(add_mod(pr, pr, Q), cr, Q);
+    }
+  }
 }

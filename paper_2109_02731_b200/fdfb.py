@@ -41,8 +41,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_bootstrap_batch_host", "fdfb_blind_rotate", "fdfb_sample_extract", "fdfb_lwe_keyswitch",
             "fdfb_vector_pack", "fdfb_shift", "fdfb_poly_mul", "fdfb_cdt_table", "fdfb_launch_count",
             "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read",
-            "fdfb_pack", "fdfb_device_status", "fdfb_key_export"]
-KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3}
+            "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming"]
+KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
 def lib():
@@ -76,6 +76,7 @@ def lib():
         L.fdfb_lwe_keyswitch.argtypes = [vp, vp, vp, vp, u32, vp]
         L.fdfb_vector_pack.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
         L.fdfb_shift.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_shift_streaming.argtypes = [vp, vp, vp, vp, vp, u32, vp]
         L.fdfb_poly_mul.argtypes = [vp, vp, vp, vp, u32, vp]
         L.fdfb_cdt_table.argtypes = [vp, vp, C.POINTER(C.c_int)]
         L.fdfb_launch_count.argtypes = [vp]
@@ -291,6 +292,12 @@ class Context:
         out = self._u64(B, 2, self.N) if out is None else out
         ws = self.workspace_shift(B) if workspace is None else workspace
         _check(lib().fdfb_shift(self.h, _ptr(pack), _ptr(rlwe), _ptr(d), _ptr(out), B, _ptr(ws), _stream(stream)))
+        return out
+
+    def shift_streaming(self, pack, rlwe, d, out=None, stream=None):
+        B = rlwe.shape[0]
+        out = self._u64(B, 2, self.N) if out is None else out
+        _check(lib().fdfb_shift_streaming(self.h, _ptr(pack), _ptr(rlwe), _ptr(d), _ptr(out), B, _stream(stream)))
         return out
 
     def poly_mul(self, a, b, stream=None):

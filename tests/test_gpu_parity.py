@@ -275,6 +275,23 @@ def test_shift_bin_path_bit_exact():
     assert np.array_equal(got, orc.shift_batch(pk, cts, ds))
 
 
+def test_shift_gemm_path_equals_streaming_kernel():
+    """The two device evaluations of Shift (int8 GEMM and CUDA-core streaming) agree byte for byte."""
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup("shift512")
+    N = cfg["N"]
+    msg = synth.rlwe_messages(cfg, 21, seed=3)
+    cts = T(orc.rlwe_encrypt(9, S, msg))
+    ds = T(synth.shift_amounts(cfg, 21, seed=4))
+    a = H(ctx.shift(dpk, cts, ds))
+    b = H(ctx.shift_streaming(dpk, cts, ds))
+    assert np.array_equal(a, b)
+    bad = T(np.array([0, 3, N], np.uint32))
+    z = H(ctx.shift(dpk, cts[:3], bad))
+    with pytest.raises(Exception):
+        ctx.device_status()
+    assert not z[0].any() and not z[2].any() and z[1].any()
+
+
 def test_shift_out_of_range_d_flagged():
     cfg, orc, s, S, pk, ctx, dpk = pack_setup("tiny_shift")
     N = cfg["N"]
@@ -319,3 +336,39 @@ def test_bootstrap_large_full_batch_noiseless_full_domain():
     ph = (out[:, 0] - (out[:, 1:] * s[None, :]).sum(axis=1)) & np.uint64(q - 1)
     dec = ((ph.astype(object) * cfg["t"] * 2 + q) // (2 * q)) % cfg["t"]
     assert [int(x) for x in dec] == [int(f[int(m)]) for m in msgs]
+
+
+@pytest.mark.slow
+def test_shift_config4_full_batch():
+    """Shift/VectorPack configuration at the bench's batch (1024 RLWE, d ~ U[1, 2047]) with the
+    oracle's PackSetup key: the items with the smallest m (the oracle's cost grows with m)
+    bit-exact with the oracle, and every output decrypts to roll(m, d) within the lemma's bound."""
+    cfg = synth.load_config("shift")
+    orc = Oracle(cfg)
+    s, S = orc.keygen_secrets(cfg["seeds"]["keys"])
+    pk = orc.pack_key(cfg["seeds"]["keys"], S)                      # ~7.25 GB, ~1.5 min on 16 threads
+    ctx = Context(cfg, 0)
+    dpk = ctx.key_import(KEY_PACK, T(pk.reshape(-1)))
+    N, Q, B = cfg["N"], cfg["Q"], cfg["batch"]
+    msg = synth.rlwe_messages(cfg, B)
+    ds = synth.shift_amounts(cfg, B)
+    cts = orc.rlwe_encrypt(cfg["seeds"]["err"], S, msg)
+    got = H(ctx.shift(dpk, T(cts), T(ds)))
+    ctx.device_status()
+    m = np.minimum(ds, N - ds)
+    for i in np.argsort(m, kind="stable")[:3]:
+        assert np.array_equal(got[i], orc.shift(pk, cts[i], int(ds[i]))), (i, ds[i])
+    Qu = np.uint64(Q)
+    worst = 0
+    for c in range(B):
+        ph = got[c, 0].copy()
+        a = got[c, 1]
+        for i in np.nonzero(S)[0]:
+            r = np.concatenate([(Qu - a[N - i:]) % Qu, a[:N - i]]) if i else a.copy()
+            if S[i] < 0:
+                r = (Qu - r) % Qu
+            ph = np.where(ph >= r, ph - r, ph + Qu - r)
+        e = (ph + Qu - np.roll(msg[c], int(ds[c]))) % Qu
+        e = np.minimum(e, Qu - e)
+        worst = max(worst, int(e.max()))
+    assert worst < Q // 1024, worst
