@@ -70,6 +70,7 @@ typedef struct fdfb_ctx fdfb_ctx;
 /* Key kinds for fdfb_key_import / fdfb_keygen_canonical. Canonical layouts:
  *   BRK  [n][u][2*ell_rgsw][2][N]   RGSW rows, row r<ell: b-gadget
  *   BPK  [N][ell_pk][2][N]          RLWE_s(s_F[i] L^j)
+ *        (device formats of BPK/KSK: the canonical table, then its int8 GEMM digits)
  *   KSK  [N][ell_ks][n+1]           LWE_s(s_F[i] L^j) mod q_lwe
  *   PACK [N][ell_pack][L_pack][2][N] RLWE_s(s_F[i] L^j k)
  *   SK_LWE int8[n], SK_RLWE int8[N]                                             */
@@ -151,9 +152,13 @@ int fdfb_blind_rotate(const fdfb_ctx* ctx, const void* brk, uint64_t* acc, const
  * launch) yields a zero row and raises the flag read by fdfb_device_status. */
 int fdfb_sample_extract(const fdfb_ctx* ctx, const uint64_t* rlwe, const uint32_t* k, uint64_t* lwe,
                         uint32_t B, void* stream);
-/* LWE KeySwitch N -> n mod q_lwe: in [dev, B x (N+1)] mod q_lwe. */
+/* LWE KeySwitch N -> n mod q_lwe: in [dev, B x (N+1)] mod q_lwe,
+ * out [dev, B x (n+1)].  With workspace [dev] of fdfb_workspace_keyswitch(ctx, B) bytes the
+ * switch runs as one exact int8 tensor-core GEMM (digit limbs x balanced base-256 key
+ * digits); with workspace NULL through the tiled CUDA-core kernel.  Same bytes. */
+size_t fdfb_workspace_keyswitch(const fdfb_ctx* ctx, uint32_t B);
 int fdfb_lwe_keyswitch(const fdfb_ctx* ctx, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
-                       uint32_t B, void* stream);
+                       uint32_t B, void* workspace, void* stream);
 /* VectorPack: lwe [dev, B x m x (N+1)] mod Q under s_F,
  * 1 <= m <= N; out [dev, B x 2N] = sum_k Pack(lwe_k, pK, k), computed by the definition
  * (m N ell key-row additions per item).  workspace may be NULL (size 0). */

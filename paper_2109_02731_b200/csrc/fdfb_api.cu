@@ -211,6 +211,108 @@ static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, in
   return FDFB_E_DIMENSION;
 }
 
+// ------------------------------------------------------------------ exact int8 GEMMs (cuBLASLt)
+// D (row-major [M][Nout] int32) = A (row-major [M][K] int8) x GK^T (GK row-major [Nout][K] int8):
+// column-major "TN" GEMM  D^T (Nout x M) = GK_cm(K x Nout)^T x A_cm(K x M).  K, Nout multiples of 16.
+static const size_t kLtWorkspace = 64ull << 20;
+static int lt_gemm_i8(const fdfb_ctx* c, const int8_t* GK, const int8_t* A, int* D, int M, int K, int Nout,
+                      void* lt_ws, int kclass, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(c->lt_mu);
+  if (!c->lt) {
+    if (cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) { g_last_cuda = "cublasLtCreate failed"; return FDFB_E_CUDA; }
+  }
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  cublasLtMatmulPreference_t pref = nullptr;
+  int rc = FDFB_OK;
+  const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+  cublasLtMatmulHeuristicResult_t heur;
+  int nres = 0;
+  const int32_t one = 1, zero = 0;
+  size_t wsb = kLtWorkspace;
+  if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, K, Nout, K) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, K, M, K) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, Nout, M, Nout) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb)) !=
+          CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulAlgoGetHeuristic(c->lt, op, la, lb, lc, lc, pref, 1, &heur, &nres) != CUBLAS_STATUS_SUCCESS ||
+      nres < 1) {
+    g_last_cuda = "cuBLASLt: no int8 TN algorithm";
+    rc = FDFB_E_CUDA;
+  } else {
+    TimedLaunch tl(c, kclass, st);
+    cublasStatus_t s = cublasLtMatmul(c->lt, op, &one, GK, la, A, lb, &zero, D, lc, D, lc, &heur.algo, lt_ws, wsb, st);
+    if (s != CUBLAS_STATUS_SUCCESS) {
+      g_last_cuda = "cublasLtMatmul failed: " + std::to_string((int)s);
+      rc = FDFB_E_CUDA;
+    }
+    c->launches++;
+  }
+  if (pref) cublasLtMatmulPreferenceDestroy(pref);
+  if (lc) cublasLtMatrixLayoutDestroy(lc);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (op) cublasLtMatmulDescDestroy(op);
+  return rc;
+}
+
+// ------------------------------------------------------------------ key switching
+static KsGemm ks_shape_rlwe(const fdfb_params& p) { return ks_gemm_shape(p.N, p.ell_pk, p.logL_pk, 2 * p.N); }
+static KsGemm ks_shape_lwe(const fdfb_params& p) { return ks_gemm_shape(p.N, p.ell_ks, p.logL_ks, p.n + 1); }
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+static const size_t kKsDBytes = 1ull << 30;     // int32 product chunk cap
+static int ks_chunk_rows(const KsGemm& g) {     // LWE samples per GEMM chunk
+  size_t r = kKsDBytes / ((size_t)g.NL * g.Nout * 4);
+  return (int)(r < 1 ? 1 : (r > (1 << 20) ? (1 << 20) : r));
+}
+static size_t ks_ws_bytes(const KsGemm& g, int count) {
+  const int rows = count < ks_chunk_rows(g) ? count : ks_chunk_rows(g);
+  return align256((size_t)rows * g.NL * g.Kd) + align256((size_t)rows * g.NL * g.Nout * 4) + kLtWorkspace;
+}
+// device formats: canonical key, then (256-aligned) its int8 digit matrix
+static size_t ks_key_bytes(size_t canon, const KsGemm& g) { return align256(canon) + (size_t)g.Nout * g.Kd; }
+static int ks_build_key(const fdfb_ctx* c, const u64* canon_dev, size_t canon_bytes, const KsGemm& g, void* dev,
+                        cudaStream_t st) {
+  if ((void*)canon_dev != dev) CK(cudaMemcpyAsync(dev, canon_dev, canon_bytes, cudaMemcpyDeviceToDevice, st));
+  int8_t* GK = (int8_t*)dev + align256(canon_bytes);
+  dim3 grd((g.Kd + 31) / 32, (g.Wpad + 7) / 8), blk(32, 8);
+  k_ks_gemm_key<<<grd, blk, 0, st>>>((const u64*)dev, g, GK);
+  CKL(c);
+  return FDFB_OK;
+}
+// out = KeySwitch(lwe) for `count` samples through the GEMM, chunked; qmask = 0 -> mod Q.
+static int ks_gemm(const fdfb_ctx* c, const void* key_dev, size_t canon_bytes, const KsGemm& g, int logL, int ell,
+                   const u64* lwe, int count, u64* out, u64 qmask, void* ws, int kclass, cudaStream_t st) {
+  const int N = c->prm.N;
+  const int8_t* GK = (const int8_t*)key_dev + align256(canon_bytes);
+  const int CH = ks_chunk_rows(g);
+  const int rows0 = count < CH ? count : CH;
+  int8_t* A = (int8_t*)ws;
+  int* D = (int*)((char*)ws + align256((size_t)rows0 * g.NL * g.Kd));
+  void* lt_ws = (char*)D + align256((size_t)rows0 * g.NL * g.Nout * 4);
+  for (int o = 0; o < count; o += CH) {
+    const int rows = (count - o) < CH ? (count - o) : CH;
+    const u64* in = lwe + (size_t)o * (N + 1);
+    dim3 gb((g.Kd + 255) / 256 < 64 ? (g.Kd + 255) / 256 : 64, rows);
+    k_ks_gemm_bits<<<gb, 256, 0, st>>>(in, rows, N, ell, logL, g, A);
+    CKL(c);
+    int rc = lt_gemm_i8(c, GK, A, D, rows * g.NL, g.Kd, g.Nout, lt_ws, kclass, st);
+    if (rc) return rc;
+    const size_t tot = (size_t)rows * g.W;
+    k_ks_gemm_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(D, in, rows, N, g, c->prm.Q, qmask,
+                                                                     out + (size_t)o * g.W);
+    CKL(c);
+  }
+  return FDFB_OK;
+}
+
+static size_t canon_bpk_bytes(const fdfb_params& p) { return (size_t)p.N * p.ell_pk * 2 * p.N * 8; }
+static size_t canon_ksk_bytes(const fdfb_params& p) { return (size_t)p.N * p.ell_ks * (p.n + 1) * 8; }
+
 // ------------------------------------------------------------------ context
 static int validate(const fdfb_params* p) {
   if (!p) return FDFB_E_NULL;
@@ -418,10 +520,10 @@ extern "C" int fdfb_sizes(const fdfb_ctx* c, fdfb_sizes_t* o) {
   o->sk_lwe = p.n; o->sk_rlwe = p.N;
   o->canon_brk = brk_words(p) * 8;
   o->brk = brk_words(p) * c->rns.np * 4;        // u32 residues per RNS prime
-  o->canon_bpk = (size_t)p.N * p.ell_pk * 2 * p.N * 8;
-  o->bpk = o->canon_bpk;
-  o->canon_ksk = (size_t)p.N * p.ell_ks * (p.n + 1) * 8;
-  o->ksk = o->canon_ksk;
+  o->canon_bpk = canon_bpk_bytes(p);
+  o->bpk = ks_key_bytes(o->canon_bpk, ks_shape_rlwe(p));      // canonical + int8 GEMM digits
+  o->canon_ksk = canon_ksk_bytes(p);
+  o->ksk = ks_key_bytes(o->canon_ksk, ks_shape_lwe(p));
   o->canon_pack = (size_t)p.N * p.ell_pack * (1ULL << p.logL_pack) * 2 * p.N * 8;
   o->pack = shift_pack_bytes(p);
   return FDFB_OK;
@@ -429,7 +531,7 @@ extern "C" int fdfb_sizes(const fdfb_ctx* c, fdfb_sizes_t* o) {
 
 // workspace layout of fdfb_bootstrap_batch
 struct BootWs {
-  u32* abar; u32* bbar; u64* accs; u64* lweN; u64* dig; u64* F; size_t bytes;
+  u32* abar; u32* bbar; u64* accs; u64* lweN; u64* dig; u64* F; void* ks; size_t bytes;
 };
 static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base) {
   BootWs w;
@@ -443,6 +545,11 @@ static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base) {
   w.lweN = (u64*)take((size_t)B * ellb * (N + 1) * 8);
   w.dig = (u64*)take((size_t)B * ellb * N * 8);
   w.F = (u64*)take((size_t)B * 2 * N * 8);
+  {
+    const size_t kr = ks_ws_bytes(ks_shape_rlwe(p), (int)(B * ellb ? B * ellb : 1));
+    const size_t kl = ks_ws_bytes(ks_shape_lwe(p), (int)(B ? B : 1));
+    w.ks = take(kr > kl ? kr : kl);
+  }
   w.bytes = off;
   return w;
 }
@@ -540,11 +647,13 @@ extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int
       int cnt = (int)((ent - o) < (size_t)CH ? (ent - o) : CH);
       rc = rlwe_entries(c, seed, 2, sk_lwe, sk_rlwe, nullptr, o, cnt, (u64*)bpk + o * 2 * N, shat, tmask, tprod, st);
     }
+    if (!rc) rc = ks_build_key(c, (const u64*)bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), bpk, st);
   }
   if (!rc && (which & 8)) {
     int ent = N * p.ell_ks;
     k_ksk_gen<<<(ent * 32 + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe, nullptr, 0, ent, (u64*)ksk);
     CKL(c);
+    rc = ks_build_key(c, (const u64*)ksk, canon_ksk_bytes(p), ks_shape_lwe(p), ksk, st);
   }
   if (!rc && (which & 16)) rc = pack_keygen(c, seed, sk_rlwe, pack, shat, tmask, tprod, tout, CH, st);
   cudaFreeAsync(shat, st); cudaFreeAsync(tmask, st); cudaFreeAsync(tprod, st); cudaFreeAsync(tout, st);
@@ -604,9 +713,9 @@ extern "C" int fdfb_key_import(const fdfb_ctx* c, int kind, const uint64_t* cano
     }
     cudaFreeAsync(tmp, st);
   } else if (kind == FDFB_KEY_BPK) {
-    CK(cudaMemcpyAsync(dev_key, canon, sz.bpk, cudaMemcpyDeviceToDevice, st));
+    rc = ks_build_key(c, canon, sz.canon_bpk, ks_shape_rlwe(p), dev_key, st);
   } else if (kind == FDFB_KEY_KSK) {
-    CK(cudaMemcpyAsync(dev_key, canon, sz.ksk, cudaMemcpyDeviceToDevice, st));
+    rc = ks_build_key(c, canon, sz.canon_ksk, ks_shape_lwe(p), dev_key, st);
   } else if (kind == FDFB_KEY_PACK) {
     rc = pack_import(c, canon, dev_key, st);
   } else {
@@ -703,14 +812,26 @@ extern "C" int fdfb_blind_rotate(const fdfb_ctx* c, const void* brk, uint64_t* a
   return launch_br(c, (const u64*)brk, acc, (int)count, (int)acc_per_ct, abar, S(stream));
 }
 
-static int keyswitch_rlwe(const fdfb_ctx* c, const u64* bpk, const u64* lwe, int count, u64* out, cudaStream_t st) {
+static int keyswitch_rlwe(const fdfb_ctx* c, const u64* bpk, const u64* lwe, int count, u64* out, void* ws,
+                          cudaStream_t st) {
+  if (ws) {
+    const fdfb_params& p = c->prm;
+    return ks_gemm(c, bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), p.logL_pk, p.ell_pk, lwe, count, out, 0, ws,
+                   FDFB_KCLASS_KEYSWITCH_RLWE, st);
+  }
   dim3 grd((2 * c->prm.N) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
   TimedLaunch tl(c, FDFB_KCLASS_KEYSWITCH_RLWE, st);
   k_keyswitch_rlwe<<<grd, KS_COLS, 0, st>>>(c->dp, bpk, lwe, count, out);
   CKL(c);
   return FDFB_OK;
 }
-static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int count, u64* out, cudaStream_t st) {
+static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int count, u64* out, void* ws,
+                         cudaStream_t st) {
+  if (ws) {
+    const fdfb_params& p = c->prm;
+    return ks_gemm(c, ksk, canon_ksk_bytes(p), ks_shape_lwe(p), p.logL_ks, p.ell_ks, lwe, count, out, c->dp.q_mask,
+                   ws, FDFB_KCLASS_KEYSWITCH_LWE, st);
+  }
   dim3 grd((c->prm.n + 1 + KS_COLS - 1) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
   TimedLaunch tl(c, FDFB_KCLASS_KEYSWITCH_LWE, st);
   k_keyswitch_lwe<<<grd, KS_COLS, 0, st>>>(c->dp, ksk, lwe, count, out);
@@ -744,7 +865,7 @@ extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const vo
   k_ladder_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.accs, B * ellb, w.lweN);
   CKL(c);
   // 5. BuildAcc: KeySwitch LWE->RLWE (into accs), PubMux
-  if ((rc = keyswitch_rlwe(c, (const u64*)bpk, w.lweN, (int)(B * ellb), w.accs, st))) return rc;
+  if ((rc = keyswitch_rlwe(c, (const u64*)bpk, w.lweN, (int)(B * ellb), w.accs, w.ks, st))) return rc;
   tot = (size_t)B * N;
   k_pubmux_digits<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, B, w.dig);
   CKL(c);
@@ -763,7 +884,7 @@ extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const vo
   tot = (size_t)B * (N + 1);
   k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.F, B, w.lweN);
   CKL(c);
-  return keyswitch_lwe(c, (const u64*)ksk, w.lweN, (int)B, ct_out, st);
+  return keyswitch_lwe(c, (const u64*)ksk, w.lweN, (int)B, ct_out, w.ks, st);
 }
 
 extern "C" int fdfb_bootstrap_batch_host(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
@@ -794,11 +915,14 @@ extern "C" int fdfb_sample_extract(const fdfb_ctx* c, const uint64_t* rlwe, cons
   return FDFB_OK;
 }
 
+extern "C" size_t fdfb_workspace_keyswitch(const fdfb_ctx* c, uint32_t B) {
+  return c ? ks_ws_bytes(ks_shape_lwe(c->prm), (int)(B ? B : 1)) : 0;
+}
 extern "C" int fdfb_lwe_keyswitch(const fdfb_ctx* c, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
-                                  uint32_t B, void* stream) {
+                                  uint32_t B, void* workspace, void* stream) {
   if (!c || !ksk || !lwe_N || !lwe_n) return FDFB_E_NULL;
   if (!B) return FDFB_OK;
-  return keyswitch_lwe(c, (const u64*)ksk, lwe_N, (int)B, lwe_n, S(stream));
+  return keyswitch_lwe(c, (const u64*)ksk, lwe_N, (int)B, lwe_n, workspace, S(stream));
 }
 
 extern "C" int fdfb_poly_mul(const fdfb_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,

@@ -1,6 +1,7 @@
 // kernels_boot.cuh -- the FDFB bootstrap hot path (Fig. Bootstrap).
 #pragma once
 #include "kernels_br.cuh"
+#include "kernels_ksgemm.cuh"
 
 // ---------------------------------------------------------------------------
 // a1: ModSwitch(ct, q_lwe, 2N) -- round half up.

@@ -41,7 +41,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_bootstrap_batch_host", "fdfb_blind_rotate", "fdfb_sample_extract", "fdfb_lwe_keyswitch",
             "fdfb_vector_pack", "fdfb_shift", "fdfb_poly_mul", "fdfb_cdt_table", "fdfb_launch_count",
             "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read",
-            "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming"]
+            "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming",
+            "fdfb_workspace_keyswitch"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -73,7 +74,9 @@ def lib():
         L.fdfb_bootstrap_batch_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_blind_rotate.argtypes = [vp, vp, vp, vp, u32, u32, vp]
         L.fdfb_sample_extract.argtypes = [vp, vp, vp, vp, u32, vp]
-        L.fdfb_lwe_keyswitch.argtypes = [vp, vp, vp, vp, u32, vp]
+        L.fdfb_lwe_keyswitch.argtypes = [vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_workspace_keyswitch.argtypes = [vp, u32]
+        L.fdfb_workspace_keyswitch.restype = sz
         L.fdfb_vector_pack.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
         L.fdfb_shift.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_shift_streaming.argtypes = [vp, vp, vp, vp, vp, u32, vp]
@@ -261,10 +264,12 @@ class Context:
         _check(lib().fdfb_sample_extract(self.h, _ptr(rlwe), _ptr(k), _ptr(out), B, _stream(stream)))
         return out
 
-    def lwe_keyswitch(self, ksk, lwe, stream=None):
+    def lwe_keyswitch(self, ksk, lwe, gemm=True, stream=None):
+        """KeySwitch N -> n; gemm=True: int8 tensor-core GEMM path, False: CUDA-core kernel."""
         B = lwe.shape[0]
         out = self._u64(B, self.n + 1)
-        _check(lib().fdfb_lwe_keyswitch(self.h, _ptr(ksk), _ptr(lwe), _ptr(out), B, _stream(stream)))
+        ws = self._bytes(lib().fdfb_workspace_keyswitch(self.h, B)) if gemm else None
+        _check(lib().fdfb_lwe_keyswitch(self.h, _ptr(ksk), _ptr(lwe), _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
 
     def vector_pack(self, pack, lwe, stream=None):

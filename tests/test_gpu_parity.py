@@ -131,9 +131,10 @@ def test_lwe_keyswitch(name):
     rng = np.random.default_rng(3)
     B = 37                                                      # ragged vs the 16-row tile
     c = rng.integers(0, 1 << cfg["log_q_lwe"], (B, cfg["N"] + 1), dtype=np.uint64)
-    got = H(ctx.lwe_keyswitch(dk["ksk"], T(c)))
+    got = H(ctx.lwe_keyswitch(dk["ksk"], T(c)))                 # int8 tensor-core GEMM path
     for i in range(0, B, 1 if name == "tiny" else 12):
         assert np.array_equal(got[i], orc.keyswitch_lwe(K["ksk"], c[i]))
+    assert np.array_equal(H(ctx.lwe_keyswitch(dk["ksk"], T(c), gemm=False)), got)   # CUDA-core kernel
 
 
 @pytest.mark.parametrize("name,count", [("tiny", 1), ("tiny", 7), ("fhew", 3)])
