@@ -138,6 +138,23 @@ int fdfb_setup_lut(const fdfb_ctx* ctx, const uint64_t* lut, uint32_t t_out, uin
 int fdfb_bootstrap_batch(const fdfb_ctx* ctx, const void* brk, const void* bpk, const void* ksk,
                          const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
                          void* workspace, void* stream);
+/* FDFB Bootstrap of B ciphertexts under k LUTs at once (rotp: [dev, k x 2 x N], one
+ * fdfb_setup_lut output per function): the ell_boot ladder rotations, their SampleExt and the
+ * LWE->RLWE key switch are computed once and reused by all k functions (PAPER.md:2568-2570:
+ * ell_boot + k blind rotations instead of k (ell_boot + 1)).  ct_out [dev, k x B x (n+1)];
+ * output kk equals fdfb_bootstrap_batch under LUT kk byte for byte.  workspace [dev] of
+ * fdfb_workspace_bootstrap_multi(ctx, B, k) bytes. */
+size_t fdfb_workspace_bootstrap_multi(const fdfb_ctx* ctx, uint32_t B, uint32_t k);
+int fdfb_bootstrap_multi_batch(const fdfb_ctx* ctx, const void* brk, const void* bpk, const void* ksk,
+                               const uint64_t* rotp, uint32_t k, const uint64_t* ct_in, uint64_t* ct_out,
+                               uint32_t B, void* workspace, void* stream);
+/* TFHE (half-domain) bootstrap (Fig. TFHE Bootstrapping PAPER.md:3070-3090, Thm 2109-2139;
+ * output order of reading c.3): one blind rotation of [rotP_0 X^{b~}, 0] (rotp [dev, 2 x N]
+ * from fdfb_setup_lut; only rotP_0 is used), SampleExt, ModSwitch Q -> q_lwe, KeySwitch.
+ * Correct for m < t/2; upper-half inputs return -F(m - t/2) (negacyclicity).  workspace of
+ * fdfb_workspace_bootstrap(ctx, B) bytes. */
+int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* ctx, const void* brk, const void* ksk, const uint64_t* rotp,
+                              const uint64_t* ct_in, uint64_t* ct_out, uint32_t B, void* workspace, void* stream);
 /* Same, with ct_in/ct_out in (pinned) HOST memory: H2D copy, bootstrap, D2H copy,
  * all on `stream`; synchronises the stream before returning. */
 int fdfb_bootstrap_batch_host(const fdfb_ctx* ctx, const void* brk, const void* bpk, const void* ksk,

@@ -538,6 +538,34 @@ void or_bootstrap(const u64* P, const u64* brk, const u64* bpk, const u64* ksk,
     bootstrap_one(P, brk, bpk, ksk, rotp0, rotp1, ct_in + (size_t)c * (n + 1), ct_out + (size_t)c * (n + 1));
 }
 
+/* ============================ TFHE (half-domain) bootstrap ======================
+ * Fig. TFHE Bootstrapping (Def./Thm 2095-2139) with the output order
+ * of reading c.3 (ModSwitch Q -> q_lwe, then KeySwitch mod q_lwe), as for FDFB:
+ *   ct_N = ModSwitch(ct, q, 2N); rotP' = rotP X^{b_N}; acc = [rotP', 0];
+ *   acc = BlindRotate(brK, acc, ct_N, u); c_Q = SampleExt(acc, 1); out = KS(ModSwitch(c_Q)). */
+static void bootstrap_tfhe_one(const u64* P, const u64* brk, const u64* ksk, const u64* rotp, const u64* ct, u64* out) {
+  int N = (int)P[P_N], n = (int)P[P_n], logq = (int)P[P_LOGQLWE]; u64 Q = P[P_Q];
+  u64 qlwe = 1ULL << logq;
+  uint32_t* abar = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t bbar = (uint32_t)or_mod_switch(ct[0], qlwe, 2 * (u64)N);          /* line 1 */
+  for (int i = 0; i < n; i++) abar[i] = (uint32_t)or_mod_switch(ct[1 + i], qlwe, 2 * (u64)N);
+  u64* acc = (u64*)calloc((size_t)2 * N, sizeof(u64));
+  or_monomial_mul(N, Q, rotp, bbar, acc);                                      /* lines 2-3 */
+  or_blind_rotate(P, brk, acc, abar, n);                                       /* line 4 */
+  u64* lwe = (u64*)malloc(sizeof(u64) * (N + 1));
+  or_sample_extract(N, Q, acc, 1, lwe);                                        /* line 5 */
+  for (int i = 0; i <= N; i++) lwe[i] = or_mod_switch(lwe[i], Q, qlwe);        /* lines 6-7, c.3 */
+  or_keyswitch_lwe(P, ksk, lwe, out);
+  free(abar); free(acc); free(lwe);
+}
+void or_bootstrap_tfhe(const u64* P, const u64* brk, const u64* ksk, const u64* rotp, const u64* ct_in, int count,
+                       u64* ct_out) {
+  int n = (int)P[P_n];
+  #pragma omp parallel for schedule(dynamic, 1) if (count > 1)
+  for (int c = 0; c < count; c++)
+    bootstrap_tfhe_one(P, brk, ksk, rotp, ct_in + (size_t)c * (n + 1), ct_out + (size_t)c * (n + 1));
+}
+
 /* ============================ Pack / VectorPack / Shift ==========================
  * Pack(c, pK, d), precomputed variant (reading G6):
  *   out = [b X^{d-1}, 0] - X^{d-1} sum_{i,j} pK[i, j, A[i,j] + 1],  A = Decomp_{L,Q}(a).

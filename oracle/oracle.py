@@ -244,6 +244,14 @@ class Oracle:
                            _p(u64(rotp[0])), _p(u64(rotp[1])), _p(cts), C.c_int(cts.shape[0]), _p(out))
         return out
 
+    def bootstrap_tfhe(self, keys, rotp0, cts):
+        """TFHE half-domain bootstrap (Fig. PAPER.md:3070-3090, output order of reading c.3)."""
+        cts = u64(cts).reshape(-1, self.n + 1)
+        out = np.zeros_like(cts)
+        lib().or_bootstrap_tfhe(_p(self.P), _p(u64(keys["brk"])), _p(u64(keys["ksk"])), _p(u64(rotp0)), _p(cts),
+                                C.c_int(cts.shape[0]), _p(out))
+        return out
+
     # ---------------------------------------------------------------- packing / shift
     def pack(self, pk, c, d):
         out = np.zeros((2, self.N), dtype=np.uint64)

@@ -174,8 +174,8 @@ static int launch_ntt_batch(const fdfb_ctx* c, u64* data, size_t count, int mode
 }
 
 template <int N, int NP>
-static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
-                       cudaStream_t st) {
+static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
+                       const u32* abar, cudaStream_t st) {
   constexpr int T = N / 8;
   const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + exchange 2 planes 9N + Garner staging 16N bytes
   static bool attr_set = false;
@@ -189,25 +189,28 @@ static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, 
   int grid = c->num_sms * per_sm;
   if (grid > n_acc) grid = n_acc;
   TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
-  k_blind_rotate<N, NP><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar);
+  k_blind_rotate<N, NP><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar);
   CKL(c);
   return FDFB_OK;
 }
+// blind-rotate n_acc accumulators; accumulator g uses mask row (g / acc_per_ct) % abar_rows
 static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
-                     cudaStream_t st) {
+                     cudaStream_t st, int abar_rows = 0) {
   if (n_acc <= 0) return FDFB_OK;
+  if (abar_rows <= 0) abar_rows = (n_acc + acc_per_ct - 1) / acc_per_ct;
   const u32* k = (const u32*)bsk;
   const bool three = c->rns.np == 3;
+#define BR_CASE(NN)                                                                                  \
+  case NN:                                                                                           \
+    return three ? launch_br_t<NN, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st)            \
+                 : launch_br_t<NN, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st);
   switch (c->prm.N) {
-    case 256: return three ? launch_br_t<256, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
-                           : launch_br_t<256, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
-    case 512: return three ? launch_br_t<512, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
-                           : launch_br_t<512, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
-    case 1024: return three ? launch_br_t<1024, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
-                            : launch_br_t<1024, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
-    case 2048: return three ? launch_br_t<2048, 3>(c, k, accs, n_acc, acc_per_ct, abar, st)
-                            : launch_br_t<2048, 2>(c, k, accs, n_acc, acc_per_ct, abar, st);
+    BR_CASE(256)
+    BR_CASE(512)
+    BR_CASE(1024)
+    BR_CASE(2048)
   }
+#undef BR_CASE
   return FDFB_E_DIMENSION;
 }
 
@@ -533,21 +536,22 @@ extern "C" int fdfb_sizes(const fdfb_ctx* c, fdfb_sizes_t* o) {
 struct BootWs {
   u32* abar; u32* bbar; u64* accs; u64* lweN; u64* dig; u64* F; void* ks; size_t bytes;
 };
-static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base) {
+static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base, uint32_t k = 1) {
   BootWs w;
   char* b = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* r = b + off; off += (bytes + 255) & ~(size_t)255; return r; };
   const size_t ellb = p.ell_boot, N = p.N;
+  const size_t nl = ellb > k ? ellb : k;                  // LWE_N samples alive at once (ladder or outputs)
   w.abar = (u32*)take((size_t)B * p.n * 4);
   w.bbar = (u32*)take((size_t)B * 4);
   w.accs = (u64*)take((size_t)B * ellb * 2 * N * 8);
-  w.lweN = (u64*)take((size_t)B * ellb * (N + 1) * 8);
+  w.lweN = (u64*)take((size_t)B * nl * (N + 1) * 8);
   w.dig = (u64*)take((size_t)B * ellb * N * 8);
-  w.F = (u64*)take((size_t)B * 2 * N * 8);
+  w.F = (u64*)take((size_t)B * k * 2 * N * 8);
   {
     const size_t kr = ks_ws_bytes(ks_shape_rlwe(p), (int)(B * ellb ? B * ellb : 1));
-    const size_t kl = ks_ws_bytes(ks_shape_lwe(p), (int)(B ? B : 1));
+    const size_t kl = ks_ws_bytes(ks_shape_lwe(p), (int)(B * k ? B * k : 1));
     w.ks = take(kr > kl ? kr : kl);
   }
   w.bytes = off;
@@ -556,6 +560,10 @@ static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base) {
 extern "C" size_t fdfb_workspace_bootstrap(const fdfb_ctx* c, uint32_t B) {
   if (!c) return 0;
   return boot_ws(c->prm, B, nullptr).bytes + (size_t)B * 2 * (c->prm.n + 1) * 8;  // + host staging
+}
+extern "C" size_t fdfb_workspace_bootstrap_multi(const fdfb_ctx* c, uint32_t B, uint32_t k) {
+  if (!c || k == 0) return 0;
+  return boot_ws(c->prm, B, nullptr, k).bytes;
 }
 
 // ------------------------------------------------------------------ encryption helpers
@@ -839,15 +847,15 @@ static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int 
   return FDFB_OK;
 }
 
-extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
-                                    const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
-                                    void* workspace, void* stream) {
-  if (!c || !brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
-  if (B == 0) return FDFB_OK;
-  cudaStream_t st = S(stream);
+// FDFB Bootstrap (Fig. Bootstrap; readings R1, F4, c.3) of B ciphertexts
+// under k LUTs (rotp: k x [2][N]); the ladder rotations, SampleExt and the LWE->RLWE key
+// switch are shared by the k functions; out: [k][B][n+1].
+static int bootstrap_impl(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk, const uint64_t* rotp,
+                          uint32_t k, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B, void* workspace,
+                          cudaStream_t st) {
   const fdfb_params& p = c->prm;
   const int N = p.N, ellb = p.ell_boot;
-  BootWs w = boot_ws(p, B, workspace);
+  BootWs w = boot_ws(p, B, workspace, k);
   int rc;
   size_t tot;
   // 1. ModSwitch(ct, q_lwe, 2N)
@@ -864,25 +872,81 @@ extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const vo
   tot = (size_t)B * ellb * (N + 1);
   k_ladder_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.accs, B * ellb, w.lweN);
   CKL(c);
-  // 5. BuildAcc: KeySwitch LWE->RLWE (into accs), PubMux
+  // 5. BuildAcc: KeySwitch LWE->RLWE (into accs), then PubMux per LUT
   if ((rc = keyswitch_rlwe(c, (const u64*)bpk, w.lweN, (int)(B * ellb), w.accs, w.ks, st))) return rc;
-  tot = (size_t)B * N;
-  k_pubmux_digits<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, B, w.dig);
-  CKL(c);
-  if ((rc = launch_ntt_batch(c, w.dig, (size_t)B * ellb, 0, st))) return rc;
   if ((rc = launch_ntt_batch(c, w.accs, (size_t)B * ellb * 2, 0, st))) return rc;
-  tot = (size_t)B * 2 * N;
-  k_pubmux_mac<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.dig, w.accs, B, w.F, c->qinv_neg, c->r2);
-  CKL(c);
-  if ((rc = launch_ntt_batch(c, w.F, (size_t)B * 2, 1, st))) return rc;
-  tot = (size_t)B * N;
-  k_pubmux_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, B, w.F);
-  CKL(c);
-  // 6. final blind rotation
-  if ((rc = launch_br(c, (const u64*)brk, w.F, (int)B, 1, w.abar, st))) return rc;
+  for (uint32_t kk = 0; kk < k; kk++) {
+    const uint64_t* rp = rotp + (size_t)kk * 2 * N;
+    u64* F = w.F + (size_t)kk * B * 2 * N;
+    tot = (size_t)B * N;
+    k_pubmux_digits<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rp, w.bbar, B, w.dig);
+    CKL(c);
+    if ((rc = launch_ntt_batch(c, w.dig, (size_t)B * ellb, 0, st))) return rc;
+    tot = (size_t)B * 2 * N;
+    k_pubmux_mac<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.dig, w.accs, B, F, c->qinv_neg, c->r2);
+    CKL(c);
+    if ((rc = launch_ntt_batch(c, F, (size_t)B * 2, 1, st))) return rc;
+    tot = (size_t)B * N;
+    k_pubmux_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rp, w.bbar, B, F);
+    CKL(c);
+  }
+  // 6. final blind rotation of all k*B accumulators in one launch
+  if ((rc = launch_br(c, (const u64*)brk, w.F, (int)(k * B), 1, w.abar, st, (int)B))) return rc;
   // 7. SampleExt(., 1), ModSwitch(Q -> q_lwe), KeySwitch mod q_lwe (reading c.3)
+  tot = (size_t)k * B * (N + 1);
+  k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.F, (int)(k * B), w.lweN);
+  CKL(c);
+  return keyswitch_lwe(c, (const u64*)ksk, w.lweN, (int)(k * B), ct_out, w.ks, st);
+}
+
+extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
+                                    const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
+                                    void* workspace, void* stream) {
+  if (!c || !brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;
+  return bootstrap_impl(c, brk, bpk, ksk, rotp, 1, ct_in, ct_out, B, workspace, S(stream));
+}
+
+extern "C" int fdfb_bootstrap_multi_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
+                                          const uint64_t* rotp, uint32_t k, const uint64_t* ct_in, uint64_t* ct_out,
+                                          uint32_t B, void* workspace, void* stream) {
+  if (!c || !brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
+  if (k == 0) return FDFB_E_DIMENSION;
+  if (B == 0) return FDFB_OK;
+  return bootstrap_impl(c, brk, bpk, ksk, rotp, k, ct_in, ct_out, B, workspace, S(stream));
+}
+
+// TFHE (half-domain) bootstrap (Fig. PAPER.md:3070-3090, output order of reading c.3):
+// acc = [rotP_0 X^{b~}, 0], one blind rotation, SampleExt, ModSwitch Q -> q_lwe, KeySwitch.
+__global__ void k_tfhe_init(DevParams p, const u64* __restrict__ rotp0, const u32* __restrict__ bbar, int B,
+                            u64* __restrict__ F) {
+  const int N = p.N;
+  const size_t total = (size_t)B * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    const int cc = (int)(x / N), j = (int)(x % N);
+    F[(size_t)cc * 2 * N + j] = rot_coeff(rotp0, j, (int)bbar[cc], N, p.Q);
+    F[(size_t)cc * 2 * N + N + j] = 0;
+  }
+}
+extern "C" int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* c, const void* brk, const void* ksk, const uint64_t* rotp,
+                                         const uint64_t* ct_in, uint64_t* ct_out, uint32_t B, void* workspace,
+                                         void* stream) {
+  if (!c || !brk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;
+  cudaStream_t st = S(stream);
+  const fdfb_params& p = c->prm;
+  const int N = p.N;
+  BootWs w = boot_ws(p, B, workspace);
+  size_t tot = (size_t)B * (p.n + 1);
+  k_modswitch_in<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct_in, B, w.abar, w.bbar);
+  CKL(c);
+  tot = (size_t)B * N;
+  k_tfhe_init<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, (int)B, w.F);
+  CKL(c);
+  int rc = launch_br(c, (const u64*)brk, w.F, (int)B, 1, w.abar, st);
+  if (rc) return rc;
   tot = (size_t)B * (N + 1);
-  k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.F, B, w.lweN);
+  k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.F, (int)B, w.lweN);
   CKL(c);
   return keyswitch_lwe(c, (const u64*)ksk, w.lweN, (int)B, ct_out, w.ks, st);
 }

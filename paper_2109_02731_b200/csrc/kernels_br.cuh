@@ -275,7 +275,7 @@ FDFB_DEV u64 shoup64_32(u32 c, u64 m, u64 ms, u64 Q) {
 template <int N, int NP>
 __global__ void __launch_bounds__(N / 8, BrShape<N>::MINB)
 k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
-               int acc_per_ct, const u32* __restrict__ abar) {
+               int acc_per_ct, int abar_rows, const u32* __restrict__ abar) {
   using S = BrShape<N>;
   constexpr int T = S::T;
   extern __shared__ u64 smem[];
@@ -296,7 +296,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
-    const u32* ab = abar + (size_t)(g / acc_per_ct) * p.n;
+    const u32* ab = abar + (size_t)((g / acc_per_ct) % abar_rows) * p.n;   // accumulator g uses abar row
 #pragma unroll 1
     for (int i = 0; i < p.n; i++) {
       const u32 ai = __ldg(ab + i);

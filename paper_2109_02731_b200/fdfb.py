@@ -42,7 +42,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_vector_pack", "fdfb_shift", "fdfb_poly_mul", "fdfb_cdt_table", "fdfb_launch_count",
             "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read",
             "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming",
-            "fdfb_workspace_keyswitch"]
+            "fdfb_workspace_keyswitch", "fdfb_workspace_bootstrap_multi", "fdfb_bootstrap_multi_batch",
+            "fdfb_bootstrap_tfhe_batch"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -75,6 +76,10 @@ def lib():
         L.fdfb_blind_rotate.argtypes = [vp, vp, vp, vp, u32, u32, vp]
         L.fdfb_sample_extract.argtypes = [vp, vp, vp, vp, u32, vp]
         L.fdfb_lwe_keyswitch.argtypes = [vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_workspace_bootstrap_multi.argtypes = [vp, u32, u32]
+        L.fdfb_workspace_bootstrap_multi.restype = sz
+        L.fdfb_bootstrap_multi_batch.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp, u32, vp, vp]
+        L.fdfb_bootstrap_tfhe_batch.argtypes = [vp, vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_workspace_keyswitch.argtypes = [vp, u32]
         L.fdfb_workspace_keyswitch.restype = sz
         L.fdfb_vector_pack.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
@@ -245,6 +250,25 @@ class Context:
         _check(lib().fdfb_bootstrap_batch(self.h, _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]),
                                           _ptr(rotp), _ptr(ct_in), _ptr(ct_out), B, _ptr(ws), _stream(stream)))
         return ct_out
+
+    def bootstrap_multi(self, keys, rotps, ct_in, workspace=None, stream=None):
+        """k LUTs on the same inputs (rotps: [k, 2, N] device tensor); returns [k, B, n+1]."""
+        B, k = ct_in.shape[0], rotps.shape[0]
+        out = self._u64(k, B, self.n + 1)
+        ws = self._bytes(lib().fdfb_workspace_bootstrap_multi(self.h, B, k)) if workspace is None else workspace
+        _check(lib().fdfb_bootstrap_multi_batch(self.h, _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]),
+                                                _ptr(rotps.contiguous()), k, _ptr(ct_in), _ptr(out), B, _ptr(ws),
+                                                _stream(stream)))
+        return out
+
+    def bootstrap_tfhe(self, keys, rotp, ct_in, workspace=None, stream=None):
+        """TFHE half-domain bootstrap with rotP_0 of rotp ([2, N] from setup_lut)."""
+        B = ct_in.shape[0]
+        out = self._u64(B, self.n + 1)
+        ws = self.workspace_bootstrap(B) if workspace is None else workspace
+        _check(lib().fdfb_bootstrap_tfhe_batch(self.h, _ptr(keys["brk"]), _ptr(keys["ksk"]), _ptr(rotp), _ptr(ct_in),
+                                               _ptr(out), B, _ptr(ws), _stream(stream)))
+        return out
 
     def bootstrap_batch_host(self, keys, rotp, ct_in_host, ct_out_host, workspace, stream=None):
         B = ct_in_host.shape[0]

@@ -373,3 +373,65 @@ def test_shift_config4_full_batch():
         e = np.minimum(e, Qu - e)
         worst = max(worst, int(e.max()))
     assert worst < Q // 1024, worst
+
+
+# ----------------------------------------------------------------------------- NEXT rows: multi-LUT, TFHE
+@pytest.mark.parametrize("B", [1, 6])
+def test_bootstrap_multi_lut_equals_single_lut_oracle(B):
+    """k LUTs sharing the ladder: output kk is byte-identical to the oracle's
+    single-LUT bootstrap under LUT kk (the reused acc_{c,i} are the same values)."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    luts = [synth.lut(cfg, seed=50 + kk) for kk in range(3)]
+    rot = torch.stack([ctx.setup_lut(f) for f in luts])
+    msgs = synth.messages(cfg, B, seed=300 + B)
+    cts = orc.lwe_encrypt(400 + B, K["s"], msgs)
+    got = H(ctx.bootstrap_multi(dk, rot, T(cts)))
+    for kk, f in enumerate(luts):
+        rotp = orc.setup_polynomial(orc.bootsmap(f))
+        assert np.array_equal(got[kk], orc.bootstrap(K, rotp, cts)), kk
+
+
+def test_bootstrap_multi_lut_large_equals_single():
+    cfg, orc, K, ctx, dk = setup("large")
+    luts = [synth.lut(cfg, seed=60 + kk) for kk in range(2)]
+    rot = torch.stack([ctx.setup_lut(f) for f in luts])
+    msgs = synth.messages(cfg, 150, seed=7)
+    cts = T(orc.lwe_encrypt(8, K["s"], msgs))
+    got = H(ctx.bootstrap_multi(dk, rot, cts))
+    for kk in range(2):
+        assert np.array_equal(got[kk], H(ctx.bootstrap_batch(dk, rot[kk], cts))), kk
+
+
+@pytest.mark.parametrize("name,B", [("tiny", 5), ("fhew", 2)])
+def test_bootstrap_tfhe_bit_exact(name, B):
+    cfg, orc, K, ctx, dk = setup(name)
+    f = synth.lut(cfg, seed=9)
+    rotp = orc.setup_polynomial(orc.bootsmap(f))
+    rot = ctx.setup_lut(f)
+    msgs = synth.messages(cfg, B, seed=11)
+    cts = orc.lwe_encrypt(12, K["s"], msgs)
+    got = H(ctx.bootstrap_tfhe(dk, rot, T(cts)))
+    assert np.array_equal(got, orc.bootstrap_tfhe(K, rotp[0], cts))
+
+
+def test_bootstrap_tfhe_negacyclic_contrast_large():
+    """Noiseless keys, mod-switch-exact inputs, Large: TFHE returns F(m) on the lower half and
+    -F(m - t/2) on the upper half, FDFB returns F(m) everywhere (SPEC.md acceptance 2)."""
+    cfg = synth.load_config("large")
+    ctx = Context(cfg, 0, noiseless=True)
+    keys = ctx.keygen(cfg["seeds"]["keys"])
+    f = synth.lut(cfg, seed=13)
+    t = cfg["t"]
+    msgs = np.arange(t, dtype=np.uint64)
+    cts = ctx.lwe_encrypt(14, keys["s"], T(msgs), exact=True)
+    rot = ctx.setup_lut(f)
+    s = H(keys["s"]).astype(np.int64).astype(np.uint64)
+    q = 1 << cfg["log_q_lwe"]
+
+    def dec(out):
+        ph = (out[:, 0] - (out[:, 1:] * s[None, :]).sum(axis=1)) & np.uint64(q - 1)
+        return [int(x) for x in ((ph.astype(object) * t * 2 + q) // (2 * q)) % t]
+
+    tf, fd = dec(H(ctx.bootstrap_tfhe(keys, rot, cts))), dec(H(ctx.bootstrap_batch(keys, rot, cts)))
+    assert fd == [int(f[m]) for m in range(t)]
+    assert tf == [int(f[m]) if m < t // 2 else (-int(f[m - t // 2])) % t for m in range(t)]

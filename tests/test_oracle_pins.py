@@ -427,3 +427,31 @@ def test_shift_l2_error_bound_noisy(toy_cfg):
         out = o.shift(pk, ct, d)
         e = [centered(int(p) - int(m), Q) for p, m in zip(o.rlwe_phase(S, out), np.roll(msg, d))]
         assert math.sqrt(sum(x * x for x in e)) <= ect + N * N * o.ell["pack"] * emax
+
+
+# ----------------------------------------------------------------------------- TFHE half-domain bootstrap
+@pytest.mark.parametrize("name", ["toy", "tiny"])
+def test_tfhe_bootstrap_half_domain_and_negacyclic_contrast(name, toy_cfg):
+    """Thm: for m <= t/2 - 1 the TFHE bootstrap decrypts to F(m); on the
+    upper half it yields -F(m - t/2) mod t (the negacyclicity the paper's method removes,
+    SPEC.md acceptance 2), while FDFB returns F(m) on the whole domain (noiseless keys,
+    mod-switch-exact inputs)."""
+    cfg = toy_cfg if name == "toy" else synth.load_config("tiny")
+    o = Oracle(cfg, noiseless=True)
+    K = o.keys(21)
+    t = o.t
+    for seed in (1, 2):
+        f = synth.lut(cfg, seed=seed)
+        r0, r1 = o.setup_polynomial(o.bootsmap(f))
+        msgs = np.arange(t, dtype=np.uint64)
+        cts = o.lwe_encrypt(31, K["s"], msgs, exact=True)
+        tf = o.bootstrap_tfhe(K, r0, cts)
+        fd = o.bootstrap(K, (r0, r1), cts)
+        for m in range(t):
+            dt = o.decode(o.lwe_phase(K["s"], tf[m]), o.q_lwe, t)
+            dfd = o.decode(o.lwe_phase(K["s"], fd[m]), o.q_lwe, t)
+            assert dfd == int(f[m]), (m, dfd)
+            if m < t // 2:
+                assert dt == int(f[m]), (m, dt)
+            else:
+                assert dt == (-int(f[m - t // 2])) % t, (m, dt)
