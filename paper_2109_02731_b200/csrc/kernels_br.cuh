@@ -71,12 +71,16 @@ FDFB_DEV u32 csub32(u32 x, u32 m) { return min(x, x - m); }
 // multiply pipe; every add here therefore carries a third, opaque zero operand z (a kernel
 // parameter the compiler cannot fold), which keeps it a 3-input IADD3 on the ALU pipe.
 // Conditional subtractions are unsigned min (VIADDMNMX).  Needs 6p < 2^32 (p < 2^29).
-FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // CT, [0, 4p)
+// Forward butterflies are lazy (no reduction): a stage adds at most 2p to the bound, so a
+// radix-8 pass maps [0, 2p) to [0, 8p) < 2^32 (p < 2^29) and one [0, 8p) -> [0, 2p)
+// reduction per value per pass (red8) replaces a conditional subtraction per butterfly.
+FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // CT, +2p per stage
   const u32 t = shoup32(Y, w, ws, p);                                   // [0, 2p)
-  const u32 x = csub32(X, p2);                                          // [0, 2p)
-  X = x + t + z;                                                        // [0, 4p)
-  Y = x - t + p2;                                                       // (0, 4p)
+  const u32 x = X;
+  X = x + t + z;
+  Y = x - t + p2;
 }
+FDFB_DEV u32 red8(u32 x, u32 p2, u32 p4) { return csub32(csub32(x, p4), p2); }   // [0, 8p) -> [0, 2p)
 FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // GS, [0, 2p)
   const u32 x = X, y = Y;
   X = csub32(x + y + z, p2);                                            // [0, 2p)
@@ -112,6 +116,10 @@ FDFB_DEV void fwd8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
 #pragma unroll
     for (int k = 0; k < 4; k++) bfw32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2, z);
   }
+#pragma unroll
+  for (int v = 0; v < V; v++)
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[v][k] = red8(x[v][k], p2, p2 + p2);
 }
 template <int V>
 FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
@@ -191,17 +199,32 @@ FDFB_DEV int qbase(int tid) { constexpr int T1 = N >> (3 * q + 3); return (tid /
 
 template <int N, int X, int V>
 FDFB_DEV void xload(u32 (&x)[V][8], const u32* sb, int base, int S) {
+  if constexpr (V == 2) {          // two polynomials per 64-bit word (layouts are conflict-free for 8-byte words too)
+    const uint2* s2 = reinterpret_cast<const uint2*>(sb);
 #pragma unroll
-  for (int v = 0; v < V; v++)
+    for (int k = 0; k < 8; k++) {
+      const uint2 v = s2[base + lay_off<N, X>(S, k)];
+      x[0][k] = v.x; x[1][k] = v.y;
+    }
+  } else {
 #pragma unroll
-    for (int k = 0; k < 8; k++) x[v][k] = sb[v * Lay<N>::WORDS + base + lay_off<N, X>(S, k)];
+    for (int v = 0; v < V; v++)
+#pragma unroll
+      for (int k = 0; k < 8; k++) x[v][k] = sb[v * Lay<N>::WORDS + base + lay_off<N, X>(S, k)];
+  }
 }
 template <int N, int X, int V>
 FDFB_DEV void xstore(const u32 (&x)[V][8], u32* sb, int base, int S) {
+  if constexpr (V == 2) {
+    uint2* s2 = reinterpret_cast<uint2*>(sb);
 #pragma unroll
-  for (int v = 0; v < V; v++)
+    for (int k = 0; k < 8; k++) s2[base + lay_off<N, X>(S, k)] = make_uint2(x[0][k], x[1][k]);
+  } else {
 #pragma unroll
-    for (int k = 0; k < 8; k++) sb[v * Lay<N>::WORDS + base + lay_off<N, X>(S, k)] = x[v][k];
+    for (int v = 0; v < V; v++)
+#pragma unroll
+      for (int k = 0; k < 8; k++) sb[v * Lay<N>::WORDS + base + lay_off<N, X>(S, k)] = x[v][k];
+  }
 }
 
 template <int N, int q, int V>
@@ -231,8 +254,8 @@ FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p,
   }
 }
 
-// Forward NTT mod p of V polynomials. In: x[v][k] = coefficient tid + T k, [0, 4p).
-// Out: slot 8 tid + k, [0, 4p).  The caller guarantees that no thread still reads sb.
+// Forward NTT mod p of V polynomials. In: x[v][k] = coefficient tid + T k, [0, 2p).
+// Out: slot 8 tid + k, [0, 8p) (lazy last pass).  The caller guarantees that no thread still reads sb.
 template <int N, int V>
 FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   using S = BrShape<N>;
@@ -360,7 +383,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
-                  const u32 xr = csub32(csub32(x[v][k], pr2), pr);       // [0, p)
+                  const u32 xr = csub32(red8(x[v][k], pr2, pr2 + pr2), pr);   // [0, 8p) -> [0, p)
                   mb[k] += (u64)xr * kb[k];                              // < 2 ell p^2 < 2^61
                   ma[k] += (u64)xr * ka[k];
                 }
@@ -447,7 +470,7 @@ k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, 
   u32* o = dev + ((step * R.np + pi) * rows_per_step + r) * 2 * (size_t)N + (size_t)col * N + 8 * tid;
 #pragma unroll
   for (int k = 0; k < 8; k++) {
-    const u32 v = csub32(csub32(x[0][k], pr2), pr);
+    const u32 v = csub32(red8(x[0][k], pr2, pr2 + pr2), pr);
     o[k] = csub32(shoup32(v, R.ninv[pi], R.ninvs[pi], pr), pr);
   }
 }
