@@ -34,6 +34,10 @@ IMAD_PER_SM_CLK = 64
 # 6 IMAD.WIDE (2 slots each) + 4 IMAD (1 slot) = 16 (SASS of tools/intbench.cu k_shoup64,
 # whose measured rate, 4 modmul/SM/clk at nominal clock, confirms it).
 IMAD_PER_MODMUL = 16
+# DRAM traffic of k_blind_rotate<2048,3> per wave of 296 resident accumulators (2 per SM), from
+# `ncu --set full` (dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/ncu_full_blind_rotate.txt):
+# the RNS brK (0.81 GB) streams about twice per wave; the kernel is integer-pipe bound.
+BR_DRAM_BYTES_PER_WAVE = 1.569e9 + 0.0126e9
 
 
 def parse():
@@ -245,8 +249,12 @@ class BootstrapWorkload:
         modmul_step = per_cmux * cmux_per_bs * self.B
         imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
         peak = 148 * IMAD_PER_SM_CLK * 1965e6
+        waves = self.B * (self.cfg["ell_boot"] + 1) / 296.0
         return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
-                "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None,
+                "unit": "T IMAD-slots/s", "frac": imad_s / peak,
+                "traffic": BR_DRAM_BYTES_PER_WAVE * waves,
+                "traffic_basis": "ncu dram bytes of one 296-accumulator wave x waves per step "
+                                 "(brK re-streamed per wave; 0.2% of HBM bandwidth, not the bound)",
                 "modmul_per_step": modmul_step, "imad_per_modmul": IMAD_PER_MODMUL,
                 "modmul_per_s": modmul_step / (kernel_ms_per_step / 1e3),
                 "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; "
