@@ -455,3 +455,78 @@ def test_tfhe_bootstrap_half_domain_and_negacyclic_contrast(name, toy_cfg):
                 assert dt == int(f[m]), (m, dt)
             else:
                 assert dt == (-int(f[m - t // 2])) % t, (m, dt)
+
+
+# ----------------------------------------------------------------------------- error-variance lemmas (one-sided)
+# Each check measures the error variance over >= 100 trials (x N coefficients) with sigma = 3.2
+# keys and compares it with the lemma's bound; 1.15x slack covers the ~4% sampling spread of a
+# variance estimate from >= 1600 samples (the bounds are nearly tight for uniform digits).
+SIG2 = 3.2 ** 2
+
+
+def _err(o, S, ct, msg):
+    return [centered(int(p) - int(m), o.Q) for p, m in zip(o.rlwe_phase(S, ct), msg)]
+
+
+def test_cmux_error_variance_bound(toy_cfg):
+    """Lemma CMux: B <= (1/3)(n+1) N ell L^2 B_C + max(B_g, B_h), n = 1."""
+    o = Oracle(toy_cfg)
+    K = o.keys(61)
+    N, L, ell = o.N, o.L["rgsw"], o.ell["rgsw"]
+    rng = np.random.default_rng(62)
+    errs = []
+    for trial in range(120):
+        i = trial % o.n
+        mg = rng.integers(0, o.Q, N, dtype=np.uint64)
+        mh = rng.integers(0, o.Q, N, dtype=np.uint64)
+        g = o.rlwe_encrypt(1000 + trial, K["S"], mg)[0]
+        h = o.rlwe_encrypt(2000 + trial, K["S"], mh)[0]
+        out = o.cmux(K["brk"][i, 0], g, h)
+        errs += _err(o, K["S"], out, mg if K["s"][i] else mh)
+    bound = (2 / 3) * N * ell * L * L * SIG2 + SIG2
+    assert np.var(errs) <= 1.15 * bound, (np.var(errs), bound)
+    assert np.var(errs) > 0.2 * bound          # the key noise is really there (not a noiseless run)
+
+
+def test_blind_rotate_error_variance_bound(toy_cfg):
+    """Lemma TFHE BlindRotate: B_out <= B_acc + (2/3) n u N ell L^2 B_brK."""
+    o = Oracle(toy_cfg)
+    K = o.keys(63)
+    N, n, L, ell = o.N, o.n, o.L["rgsw"], o.ell["rgsw"]
+    rng = np.random.default_rng(64)
+    errs = []
+    for trial in range(120):
+        m = rng.integers(0, o.Q, N, dtype=np.uint64)
+        acc = np.zeros((2, N), np.uint64); acc[0] = m                   # trivial, B_acc = 0
+        abar = rng.integers(0, 2 * N, n).astype(np.uint32)
+        out = o.blind_rotate(K["brk"], acc, abar)
+        e = -sum(int(x) * int(y) for x, y in zip(abar, K["s"]))
+        errs += _err(o, K["S"], out, o.monomial_mul(m, e))
+    bound = (2 / 3) * n * o.u * N * ell * L * L * SIG2
+    assert np.var(errs) <= 1.15 * bound, (np.var(errs), bound)
+
+
+def test_keyswitch_error_variance_bounds(toy_cfg):
+    """Lemma KeySwitch: B <= B_c + (1/3) n ell L^2 B_ksK, for the LWE->LWE
+    switch with ksK (n = N inputs, mod q_lwe) and the LWE->RLWE switch with pK (mod Q)."""
+    o = Oracle(toy_cfg)
+    K = o.keys(65)
+    N = o.N
+    rng = np.random.default_rng(66)
+    el, er = [], []
+    for trial in range(150):
+        a = rng.integers(0, o.q_lwe, N, dtype=np.uint64)
+        mu = int(rng.integers(0, o.q_lwe))
+        b = (sum(int(x) * int(y) for x, y in zip(a, K["S"])) + mu) % o.q_lwe       # noiseless input
+        ph = o.lwe_phase(K["s"], o.keyswitch_lwe(K["ksk"], np.concatenate([[b], a]).astype(np.uint64)))
+        d = (ph - mu) % o.q_lwe
+        el.append(d - o.q_lwe if d > o.q_lwe // 2 else d)
+        aq = rng.integers(0, o.Q, N, dtype=np.uint64)
+        muq = int(rng.integers(0, o.Q))
+        bq = (sum(int(x) * int(y) for x, y in zip(aq, K["S"])) + muq) % o.Q
+        out = o.keyswitch_rlwe(K["bpk"], np.concatenate([[bq], aq]).astype(np.uint64))
+        er += _err(o, K["S"], out, [muq] + [0] * (N - 1))
+    bl = (1 / 3) * N * o.ell["ks"] * o.L["ks"] ** 2 * SIG2
+    br = (1 / 3) * N * o.ell["pk"] * o.L["pk"] ** 2 * SIG2
+    assert np.var(el) <= 1.25 * bl, (np.var(el), bl)          # 150 samples: wider sampling spread
+    assert np.var(er) <= 1.15 * br, (np.var(er), br)
