@@ -195,6 +195,16 @@ int fdfb_pack(const fdfb_ctx* ctx, const void* pack, const uint64_t* lwe, const 
  * fdfb_device_status flag. */
 int fdfb_shift(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* d,
                uint64_t* rlwe_out, uint32_t B, void* workspace, void* stream);
+/* Permute (reading P1: v[j] = Pack(SampleExt(ct, j), pK, 1)):
+ * rlwe_in [dev, B x 2N] encrypting m, perm [dev, B x N] with perm[i-1] = pi(i) (1-based, a
+ * permutation of 1..N) -> rlwe_out [dev, B x 2N] encrypting sum_i m_{pi(i)} X^{i-1}.  For
+ * L_pack = 2 every moved slot is one row of an exact int8 tensor-core GEMM against the digits
+ * of pK[.,.,1] - pK[.,.,0] (workspace [dev] of fdfb_workspace_permute(ctx, B) bytes
+ * required); otherwise the definition is evaluated directly (workspace may be NULL).  An
+ * entry outside 1..N is treated as a fixed point and raises the fdfb_device_status flag. */
+size_t fdfb_workspace_permute(const fdfb_ctx* ctx, uint32_t B);
+int fdfb_permute(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* perm,
+                 uint64_t* rlwe_out, uint32_t B, void* workspace, void* stream);
 /* The same Shift through the streaming (CUDA-core) kernel for any L_pack; no workspace. */
 int fdfb_shift_streaming(const fdfb_ctx* ctx, const void* pack, const uint64_t* rlwe_in, const uint32_t* d,
                          uint64_t* rlwe_out, uint32_t B, void* stream);

@@ -629,6 +629,46 @@ void or_shift_batch(const u64* P, const u64* pack, const u64* ct, const uint32_t
     or_shift(P, pack, ct + (size_t)c * 2 * N, (int)d[c], 0, out + (size_t)c * 2 * N);
 }
 
+/* Permute(ct, pK, pi), reading P1: step 1.a packs the extracted sample
+ * into slot 1, v[j] = Pack(SampleExt(ct, j), pK, 1) (message at X^0) -- with the printed
+ * "Pack(., pK, j)" step 3.a would move m_j to X^{i+j-2} and the lemma fails.
+ *   1. for i in [N] with pi(i) = j != i: v[j] = Pack(SampleExt(ct, j), pK, 1)
+ *   2. ct_out = ct
+ *   3. for i in [N] with pi(i) = j != i: ct_out += (v[j] - v[i]) X^{i-1}
+ * perm[i-1] = pi(i) (1-based values).  literal != 0 uses the printed Pack(., pK, j) instead
+ * (for the test that shows the reading is needed). */
+void or_permute(const u64* P, const u64* pack, const u64* ct, const uint32_t* perm, int literal, u64* out) {
+  int N = (int)P[P_N]; u64 Q = P[P_Q];
+  u64* v = (u64*)calloc((size_t)N * 2 * N, sizeof(u64));
+  u64* lwe = (u64*)malloc(sizeof(u64) * (N + 1));
+  for (int i = 1; i <= N; i++) {
+    int j = (int)perm[i - 1];
+    if (j == i) continue;
+    or_sample_extract(N, Q, ct, j, lwe);
+    or_pack(P, pack, lwe, literal ? j : 1, v + (size_t)(j - 1) * 2 * N);
+  }
+  memcpy(out, ct, sizeof(u64) * 2 * N);
+  u64* t = (u64*)malloc(sizeof(u64) * 2 * N);
+  for (int i = 1; i <= N; i++) {
+    int j = (int)perm[i - 1];
+    if (j == i) continue;
+    const u64* vj = v + (size_t)(j - 1) * 2 * N;
+    const u64* vi = v + (size_t)(i - 1) * 2 * N;
+    for (int h = 0; h < 2; h++) {
+      poly_sub(N, Q, vj + h * N, vi + h * N, t + h * N);
+      or_monomial_mul(N, Q, t + h * N, i - 1, t + h * N);
+      poly_add(N, Q, out + h * N, t + h * N, out + h * N);
+    }
+  }
+  free(v); free(lwe); free(t);
+}
+void or_permute_batch(const u64* P, const u64* pack, const u64* ct, const uint32_t* perm, int count, u64* out) {
+  int N = (int)P[P_N];
+  #pragma omp parallel for schedule(dynamic, 1) if (count > 1)
+  for (int c = 0; c < count; c++)
+    or_permute(P, pack, ct + (size_t)c * 2 * N, perm + (size_t)c * N, 0, out + (size_t)c * 2 * N);
+}
+
 /* RLWE encryption of a batch of message polynomials (Shift inputs), domain 8. */
 void or_rlwe_encrypt_batch(const u64* P, u64 seed, const int8_t* s, const u64* msgs, int count, u64* out) {
   int N = (int)P[P_N];

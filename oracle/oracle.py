@@ -270,6 +270,20 @@ class Oracle:
                        C.c_int(1 if force_branch2 else 0), _p(out))
         return out
 
+    def permute(self, pk, ct, perm, literal=False):
+        """Permute(ct, pK, pi) (reading P1); perm[i-1] = pi(i), 1-based."""
+        out = np.zeros((2, self.N), dtype=np.uint64)
+        perm = np.ascontiguousarray(np.asarray(perm, dtype=np.uint32))
+        lib().or_permute(_p(self.P), _p(u64(pk)), _p(u64(ct)), _p(perm), C.c_int(1 if literal else 0), _p(out))
+        return out
+
+    def permute_batch(self, pk, cts, perms):
+        cts = u64(cts).reshape(-1, 2, self.N)
+        perms = np.ascontiguousarray(np.asarray(perms, dtype=np.uint32)).reshape(-1, self.N)
+        out = np.zeros_like(cts)
+        lib().or_permute_batch(_p(self.P), _p(u64(pk)), _p(cts), _p(perms), C.c_int(cts.shape[0]), _p(out))
+        return out
+
     def shift_batch(self, pk, cts, ds):
         cts = u64(cts).reshape(-1, 2, self.N)
         ds = np.ascontiguousarray(np.asarray(ds, dtype=np.uint32))

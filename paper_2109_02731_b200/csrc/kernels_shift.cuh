@@ -8,7 +8,8 @@
 //   U   sum_j sum_{i>=2} T^{(0)}_{i,j}   [2][N]
 //   Uj  per-j partials of U              [ell][2][N]
 //   S0  sum_j T^{(0)}_{1,j}              [2][N]        (L == 2: Shift-as-GEMM key below)
-//   GK  int8 [7 * 2N][Kpad] balanced base-256 digits of the GEMM key matrix
+//   GK  int8 [7 * 2N][Kpad] balanced base-256 digits of the Shift GEMM key matrix
+//   GP  int8 [7 * 2N][N ell] digits of Delta0_{k,l} = pK[k,l,1] - pK[k,l,0] (Permute GEMM)
 // with the key-only suffix sums  T^{(v)}_{i,j} = sum_{i'>=i} X^{i'-i} pK[i',j,v]  and
 // Delta^{(v)}_{i,j} = T^{(v)}_{i,j} - T^{(0)}_{i,j}.
 //
@@ -26,7 +27,7 @@
 struct PackLayout {
   size_t P;                 // words per RLWE (2N)
   size_t A, T1, D, U, Uj;   // word offsets
-  size_t S0, GK;            // L == 2 only: S0 = sum_j T^(0)_{1,j} [2][N]; GEMM key digits (int8, see below)
+  size_t S0, GK, GP;        // L == 2 only: S0 = sum_j T^(0)_{1,j} [2][N]; Shift / Permute GEMM key digits (int8)
   size_t words;
 };
 static inline size_t shift_gemm_key_bytes(int N, int ell, int L) {
@@ -44,7 +45,8 @@ static inline PackLayout pack_layout(int N, int ell, int L) {
   l.Uj = l.U + l.P;
   l.S0 = l.Uj + (size_t)ell * l.P;
   l.GK = l.S0 + l.P;
-  l.words = l.GK + (shift_gemm_key_bytes(N, ell, L) + 7) / 8;
+  l.GP = l.GK + (shift_gemm_key_bytes(N, ell, L) + 7) / 8;
+  l.words = l.GP + ((L == 2 ? (size_t)14 * N * (size_t)N * ell : 0) + 7) / 8;
   return l;
 }
 
@@ -499,4 +501,141 @@ k_shift_gemm_finish(DevParams p, const u64* __restrict__ pk, PackLayout lay, con
       o[x] = sub_mod(add_mod(pr, pr, Q), cr, Q);
     }
   }
+}
+
+// ===========================================================================
+// Permute(ct, pK, pi) (reading P1: v[j] = Pack(SampleExt(ct, j), pK, 1)):
+//   ct_out = ct + sum_{i : pi(i) = j != i} X^{i-1} (v[j] - v[i]),
+//   v[j] - v[i] = [b_j - b_i, 0] - sum_{k,l} (pK[k,l,A_j[k,l]] - pK[k,l,A_i[k,l]])
+// (A_j = Decomp(SampleExt(ct, j).a); the constant pK[.,.,0] parts cancel for L = 2).
+// L == 2: every moved slot i is one GEMM row with coefficients A_j - A_i in {-1, 0, 1} against
+// the key matrix of Delta0_{k,l} = pK[k,l,1] - pK[k,l,0] (7 balanced base-256 digits, int8),
+// exact in int32 (|sum| <= N ell 128 < 2^31); k_permute_finish recombines, rotates and adds.
+struct PermGemm { int K; int Nout; };          // K = N ell (multiple of 16), Nout = 7 * 2N
+static inline PermGemm perm_gemm_shape(int N, int ell) { PermGemm g; g.K = N * ell; g.Nout = 14 * N; return g; }
+static inline size_t perm_gemm_key_bytes(int N, int ell, int L) {
+  return L == 2 ? (size_t)14 * N * (size_t)N * ell : 0;
+}
+// GP[l * 2N + w][k*ell + j] = digit l of Delta0_{k,j}[w]
+__global__ void k_perm_gemm_key(DevParams p, const u64* __restrict__ pk, PackLayout lay, PermGemm g,
+                                int8_t* __restrict__ GP) {
+  const int kk = blockIdx.x * 32 + threadIdx.x;   // (k, j) row of the canonical table
+  const int w = blockIdx.y * 8 + threadIdx.y;
+  if (kk >= g.K || w >= 2 * p.N) return;
+  const u64* e = pk + lay.A + (size_t)kk * 2 * lay.P;                    // pK[k,j,0], then pK[k,j,1]
+  u64 v = sub_mod(e[lay.P + w], e[w], p.Q);
+#pragma unroll
+  for (int l = 0; l < 7; l++) {
+    int t = (int)(v & 255);
+    if (t >= 128) t -= 256;
+    v = (u64)((long long)v - t) >> 8;
+    GP[((size_t)l * 2 * p.N + w) * g.K + kk] = (int8_t)t;
+  }
+}
+// rows r = c_local * N + (i-1) of a chunk of ciphertexts: A[r][k*ell + l] = bit_l(a'_j[k]) - bit_l(a'_i[k]),
+// j = pi(i); zero rows for fixed points (and flag an invalid permutation entry).
+__global__ void k_perm_bits(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, int nct,
+                            PermGemm g, int8_t* __restrict__ A, int* __restrict__ status) {
+  const int N = p.N, ell = p.ell_pack;
+  const int r = blockIdx.y;                         // local row
+  const int c = c0 + r / N, i = r % N + 1;          // 1-based slot
+  int j = (int)perm[(size_t)c * N + (i - 1)];
+  if (j < 1 || j > N) { if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, 1); j = i; }
+  const u64* a = ct + (size_t)c * 2 * N + N;
+  int8_t* row = A + (size_t)r * g.K;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.K; x += gridDim.x * blockDim.x) {
+    int8_t v = 0;
+    if (j != i) {
+      const int k = x / ell + 1, l = x % ell;       // SampleExt index k (1-based), bit l
+      const int bj = (int)((sx_mask(a, j, k, N, p.Q) >> l) & 1), bi = (int)((sx_mask(a, i, k, N, p.Q) >> l) & 1);
+      v = (int8_t)(bj - bi);
+    }
+    row[x] = v;
+  }
+}
+// out[c] = ct[c] + sum_{i moved} X^{i-1} ([b_j - b_i, 0] - W_i), one CTA per (ciphertext, column)
+template <int CPT>
+__global__ void __launch_bounds__(256)
+k_permute_finish(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, PermGemm g,
+                 const int* __restrict__ D, u64* __restrict__ out) {
+  constexpr int TPB = 256;
+  const int N = p.N, cl = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int c = c0 + cl;
+  const u64 Q = p.Q;
+  __shared__ u64 W[2048];
+  const u64* cth = ct + (size_t)c * 2 * N;
+  u64 acc[CPT];
+#pragma unroll
+  for (int r = 0; r < CPT; r++) acc[r] = cth[(size_t)h * N + tid + r * TPB];
+  for (int i = 1; i <= N; i++) {
+    int j = (int)perm[(size_t)c * N + (i - 1)];
+    if (j < 1 || j > N || j == i) continue;                      // uniform across the CTA
+    const int* drow = D + ((size_t)cl * N + (i - 1)) * g.Nout + (size_t)h * N;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) {
+      const int x = tid + r * TPB;
+      __int128 v = 0;
+#pragma unroll
+      for (int l = 6; l >= 0; l--) v = v * 256 + drow[(size_t)l * 2 * N + x];
+      long long m = (long long)(v % (__int128)Q);
+      u64 t = neg_mod((u64)(m < 0 ? m + (long long)Q : m), Q);     // -W_i
+      if (h == 0 && x == 0) t = add_mod(t, sub_mod(cth[j - 1], cth[i - 1], Q), Q);   // + [b_j - b_i, 0]
+      W[x] = t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) acc[r] = add_mod(acc[r], rot_coeff(W, tid + r * TPB, i - 1, N, Q), Q);
+  }
+#pragma unroll
+  for (int r = 0; r < CPT; r++) out[(size_t)c * 2 * N + (size_t)h * N + tid + r * TPB] = acc[r];
+}
+// Definition path for any L (small N): per (ciphertext, column) CTA, every moved slot's
+// v[j] - v[i] gathered from the canonical table, rotated by X^{i-1} and added.
+template <int CPT>
+__global__ void __launch_bounds__(256)
+k_permute_direct(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ ct,
+                 const u32* __restrict__ perm, u64* __restrict__ out, int* __restrict__ status) {
+  constexpr int TPB = 256;
+  const int N = p.N, c = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int ell = p.ell_pack, logL = p.logL_pack, L = 1 << logL;
+  const u64 Q = p.Q, dmask = (u64)L - 1;
+  __shared__ u64 W[2048];
+  const u64* cth = ct + (size_t)c * 2 * N;
+  const u64* a = cth + N;
+  u64 acc[CPT];
+#pragma unroll
+  for (int r = 0; r < CPT; r++) acc[r] = cth[(size_t)h * N + tid + r * TPB];
+  for (int i = 1; i <= N; i++) {
+    int j = (int)perm[(size_t)c * N + (i - 1)];
+    if (j < 1 || j > N) { if (tid == 0 && h == 0) atomicOr(status, 1); continue; }
+    if (j == i) continue;
+    u64 s[CPT];
+#pragma unroll
+    for (int r = 0; r < CPT; r++) s[r] = 0;
+    for (int k = 1; k <= N; k++) {
+      const u64 aj = sx_mask(a, j, k, N, Q), ai = sx_mask(a, i, k, N, Q);
+      for (int l = 0; l < ell; l++) {
+        const u64 vj = (aj >> (l * logL)) & dmask, vi = (ai >> (l * logL)) & dmask;
+        if (vj == vi) continue;
+        const u64* rj = pk + lay.A + (((size_t)(k - 1) * ell + l) * L + vj) * lay.P + (size_t)h * N + tid;
+        const u64* ri = pk + lay.A + (((size_t)(k - 1) * ell + l) * L + vi) * lay.P + (size_t)h * N + tid;
+#pragma unroll
+        for (int r = 0; r < CPT; r++) s[r] = add_mod(s[r], sub_mod(__ldg(ri + r * TPB), __ldg(rj + r * TPB), Q), Q);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) {
+      const int x = tid + r * TPB;
+      u64 t = s[r];                                                  // -(sum pK[.,A_j] - sum pK[.,A_i])
+      if (h == 0 && x == 0) t = add_mod(t, sub_mod(cth[j - 1], cth[i - 1], Q), Q);
+      W[x] = t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CPT; r++) acc[r] = add_mod(acc[r], rot_coeff(W, tid + r * TPB, i - 1, N, Q), Q);
+  }
+#pragma unroll
+  for (int r = 0; r < CPT; r++) out[(size_t)c * 2 * N + (size_t)h * N + tid + r * TPB] = acc[r];
 }

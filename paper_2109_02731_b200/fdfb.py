@@ -43,7 +43,7 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read",
             "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming",
             "fdfb_workspace_keyswitch", "fdfb_workspace_bootstrap_multi", "fdfb_bootstrap_multi_batch",
-            "fdfb_bootstrap_tfhe_batch"]
+            "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -80,6 +80,9 @@ def lib():
         L.fdfb_workspace_bootstrap_multi.restype = sz
         L.fdfb_bootstrap_multi_batch.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp, u32, vp, vp]
         L.fdfb_bootstrap_tfhe_batch.argtypes = [vp, vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_workspace_permute.argtypes = [vp, u32]
+        L.fdfb_workspace_permute.restype = sz
+        L.fdfb_permute.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_workspace_keyswitch.argtypes = [vp, u32]
         L.fdfb_workspace_keyswitch.restype = sz
         L.fdfb_vector_pack.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
@@ -321,6 +324,16 @@ class Context:
         out = self._u64(B, 2, self.N) if out is None else out
         ws = self.workspace_shift(B) if workspace is None else workspace
         _check(lib().fdfb_shift(self.h, _ptr(pack), _ptr(rlwe), _ptr(d), _ptr(out), B, _ptr(ws), _stream(stream)))
+        return out
+
+    def permute(self, pack, rlwe, perm, out=None, stream=None):
+        """Permute slots: out encrypts sum_i m_{perm[i-1]} X^{i-1} (perm: [B, N] uint32, 1-based)."""
+        B = rlwe.shape[0]
+        out = self._u64(B, 2, self.N) if out is None else out
+        n = lib().fdfb_workspace_permute(self.h, B)
+        ws = self._bytes(n) if n else None
+        _check(lib().fdfb_permute(self.h, _ptr(pack), _ptr(rlwe), _ptr(perm), _ptr(out), B, _ptr(ws),
+                                  _stream(stream)))
         return out
 
     def shift_streaming(self, pack, rlwe, d, out=None, stream=None):

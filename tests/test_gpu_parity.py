@@ -435,3 +435,25 @@ def test_bootstrap_tfhe_negacyclic_contrast_large():
     tf, fd = dec(H(ctx.bootstrap_tfhe(keys, rot, cts))), dec(H(ctx.bootstrap_batch(keys, rot, cts)))
     assert fd == [int(f[m]) for m in range(t)]
     assert tf == [int(f[m]) if m < t // 2 else (-int(f[m - t // 2])) % t for m in range(t)]
+
+
+# ----------------------------------------------------------------------------- Permute (NEXT #3)
+@pytest.mark.parametrize("name", ["tiny_shift", "shift512"])
+def test_permute_bit_exact(name):
+    """Permute (reading P1) on the definition path (L = 512) and the int8 GEMM
+    path (L = 2, ell = 54): identity, a transposition, a rotation and random permutations."""
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup(name)
+    N = cfg["N"]
+    rng = np.random.default_rng(23)
+    perms = [np.arange(1, N + 1), np.roll(np.arange(1, N + 1), 5)]
+    p2 = np.arange(1, N + 1); p2[[0, N - 1]] = p2[[N - 1, 0]]
+    perms += [p2, rng.permutation(N) + 1, rng.permutation(N) + 1]
+    perms = np.stack(perms).astype(np.uint32)
+    msg = synth.rlwe_messages(cfg, len(perms), seed=24)
+    cts = orc.rlwe_encrypt(25, S, msg)
+    got = H(ctx.permute(dpk, T(cts), T(perms)))
+    ctx.device_status()
+    assert np.array_equal(got, orc.permute_batch(pk, cts, perms))
+    ph = orc.rlwe_phase(S, got[3])                       # decrypts to the permuted message
+    e = (ph.astype(object) - msg[3][perms[3] - 1].astype(object)) % cfg["Q"]
+    assert max(min(int(x), cfg["Q"] - int(x)) for x in e) < cfg["Q"] // 1024

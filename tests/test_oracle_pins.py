@@ -530,3 +530,23 @@ def test_keyswitch_error_variance_bounds(toy_cfg):
     br = (1 / 3) * N * o.ell["pk"] * o.L["pk"] ** 2 * SIG2
     assert np.var(el) <= 1.25 * bl, (np.var(el), bl)          # 150 samples: wider sampling spread
     assert np.var(er) <= 1.15 * br, (np.var(er), br)
+
+
+
+# ----------------------------------------------------------------------------- Permute (NEXT #3)
+def test_permute_lemma_and_reading(toy_pack):
+    """Lemma Permute: m_out = sum_i m_{pi(i)} X^{i-1} for any permutation,
+    with reading P1 (Pack into slot 1); the printed Pack(., pK, j) breaks the lemma."""
+    o, S, pk = toy_pack
+    rng = np.random.default_rng(17)
+    msg = rng.integers(0, o.Q, o.N, dtype=np.uint64)
+    ct = o.rlwe_encrypt(45, S, msg)[0]
+    perms = [np.arange(1, o.N + 1), np.roll(np.arange(1, o.N + 1), 3), np.arange(o.N, 0, -1)]
+    perms += [rng.permutation(o.N) + 1 for _ in range(4)]
+    p2 = np.arange(1, o.N + 1); p2[[2, 9]] = p2[[9, 2]]               # one transposition
+    perms.append(p2)
+    for perm in perms:
+        out = o.permute(pk, ct, perm)
+        assert np.array_equal(o.rlwe_phase(S, out), msg[np.asarray(perm) - 1])
+    bad = o.permute(pk, ct, perms[1], literal=True)
+    assert not np.array_equal(o.rlwe_phase(S, bad), msg[perms[1] - 1])
