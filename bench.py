@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="end-to-end steps (default: --steps)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (GPU box); gloo only for functional tests")
     a = ap.parse_args()
     if a.config is None:
         a.config = "shift" if a.workload == "shift" else "large"
@@ -160,6 +161,8 @@ def cpu_oracle_sample(cfg, seconds):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if world > 1:   # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 alone runs the oracle here
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     import synth
     cfg = synth.load_config(args.config)
     vals = []
@@ -379,10 +382,17 @@ def main():
     from paper_2109_02731_b200 import Context
     from paper_2109_02731_b200.dist import max_over_ranks
 
+    # FDFB_SHARE_DEVICE=1 maps every rank to device 0: a functional test of the multi-rank path
+    # on a one-GPU box (ranks never wait on each other inside kernels); not for measurements.
+    if os.environ.get("FDFB_SHARE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     cfg = synth.load_config(args.config)
     B = args.batch or cfg["batch"]
     ctx = Context(cfg, local)

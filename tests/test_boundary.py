@@ -59,3 +59,25 @@ def test_binding_fails_loudly_without_cuda():
     from paper_2109_02731_b200 import Context, FdfbError
     with pytest.raises(FdfbError):
         Context(synth.load_config("tiny"))
+
+
+def test_parameter_validation_before_device_use():
+    """fdfb_ctx_create validates every parameter before touching a device (status codes, no throw)."""
+    import synth
+    from paper_2109_02731_b200 import build
+    from paper_2109_02731_b200.fdfb import params_from_config
+    lib = ctypes.CDLL(build.build())
+    base = synth.load_config("large")
+
+    def rc(**kw):
+        cfg = dict(base, **kw)
+        h = ctypes.c_void_p()
+        return lib.fdfb_ctx_create(ctypes.byref(params_from_config(cfg)), 0, ctypes.byref(h))
+
+    assert rc(N=3000) == -3                                   # N not a power of two in range
+    assert rc(Q=base["Q"] + 2) == -2                          # not prime
+    assert rc(Q=2**31 - 1) == -2                              # prime, but not 1 mod 2N
+    assert rc(ell_rgsw=3) == -4                               # ell != ceil(54 / 14)
+    assert rc(ell_ks=12) == -4
+    assert rc(t=3) == -6                                      # t does not divide 2N
+    assert rc(n=0) == -3

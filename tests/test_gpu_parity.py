@@ -457,3 +457,15 @@ def test_permute_bit_exact(name):
     ph = orc.rlwe_phase(S, got[3])                       # decrypts to the permuted message
     e = (ph.astype(object) - msg[3][perms[3] - 1].astype(object)) % cfg["Q"]
     assert max(min(int(x), cfg["Q"] - int(x)) for x in e) < cfg["Q"] // 1024
+
+
+def test_bootstrap_host_buffers_api():
+    """fdfb_bootstrap_batch_host (pinned host in/out, copies on the stream) == the device call."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    f = synth.lut(cfg, seed=71)
+    rot = ctx.setup_lut(f)
+    cts = orc.lwe_encrypt(72, K["s"], synth.messages(cfg, 9, seed=73))
+    h_in = torch.from_numpy(cts).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    ctx.bootstrap_batch_host(dk, rot, h_in, h_out, ctx.workspace_bootstrap(9))
+    assert np.array_equal(h_out.numpy(), H(ctx.bootstrap_batch(dk, rot, T(cts))))
