@@ -328,7 +328,7 @@ static int validate(const fdfb_params* p) {
   auto ok = [](uint32_t logL, uint32_t ell, int bits) {
     return logL >= 1 && logL <= 32 && ell >= 1 && (int)ell == (bits + (int)logL - 1) / (int)logL;
   };
-  if (!ok(p->logL_rgsw, p->ell_rgsw, qb) || p->ell_rgsw > 8) return FDFB_E_DECOMP;
+  if (!ok(p->logL_rgsw, p->ell_rgsw, qb) || p->ell_rgsw > 8 || p->logL_rgsw > 27) return FDFB_E_DECOMP;  // digits < RNS primes
   if (!ok(p->logL_boot, p->ell_boot, qb) || p->ell_boot > 64) return FDFB_E_DECOMP;
   if (!ok(p->logL_pk, p->ell_pk, qb)) return FDFB_E_DECOMP;
   if (!ok(p->logL_ks, p->ell_ks, (int)p->log_q_lwe)) return FDFB_E_DECOMP;
@@ -384,7 +384,7 @@ static u64 h_primroot_2n(u64 pr, int N) {
   }
   return 0;
 }
-// Choose the RNS primes (largest p < 2^29 so that 6p < 2^32, p = 1 mod 2N) so that prod p > 2 * bound + 1 with
+// Choose the RNS primes (largest p < 2^28 so that 16p < 2^32, p = 1 mod 2N) so that prod p > 2 * bound + 1 with
 // bound = 2 ell N (L-1) (Q-1) >= |coefficients| of sum_r D_r * K_r; build constants/tables.
 static int setup_rns(fdfb_ctx* c) {
   const fdfb_params& p = c->prm;
@@ -394,9 +394,9 @@ static int setup_rns(fdfb_ctx* c) {
   const u128 bound = (u128)(2 * p.ell_rgsw) * N * ((1ULL << p.logL_rgsw) - 1) * (p.Q - 1);
   std::vector<u64> primes;
   u128 P = 1;
-  for (u64 cand = ((1ULL << 29) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 28) && primes.size() < RNS_MAXP;
+  for (u64 cand = ((1ULL << 28) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 27) && primes.size() < RNS_MAXP;
        cand -= 2 * (u64)N) {
-    if (cand >= (1ULL << 29) || cand == p.Q || !h_is_prime(cand)) continue;
+    if (cand >= (1ULL << 28) || cand == p.Q || !h_is_prime(cand)) continue;
     primes.push_back(cand);
     P *= cand;
     if (primes.size() >= 2 && P / 2 > bound + 1) break;

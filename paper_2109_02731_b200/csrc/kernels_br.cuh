@@ -71,9 +71,10 @@ FDFB_DEV u32 csub32(u32 x, u32 m) { return min(x, x - m); }
 // multiply pipe; every add here therefore carries a third, opaque zero operand z (a kernel
 // parameter the compiler cannot fold), which keeps it a 3-input IADD3 on the ALU pipe.
 // Conditional subtractions are unsigned min (VIADDMNMX).  Needs 6p < 2^32 (p < 2^29).
-// Forward butterflies are lazy (no reduction): a stage adds at most 2p to the bound, so a
-// radix-8 pass maps [0, 2p) to [0, 8p) < 2^32 (p < 2^29) and one [0, 8p) -> [0, 2p)
-// reduction per value per pass (red8) replaces a conditional subtraction per butterfly.
+// Forward butterflies are lazy (no reduction): a stage adds at most 2p to the bound.  With
+// p < 2^28 values may grow to 16p < 2^32, so the transform tracks its bound at compile time
+// and reduces (red16, [0, 16p) -> [0, 2p)) only before a pass that would overflow: once per
+// 2048-point transform instead of a conditional subtraction per butterfly.
 FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // CT, +2p per stage
   const u32 t = shoup32(Y, w, ws, p);                                   // [0, 2p)
   const u32 x = X;
@@ -81,6 +82,9 @@ FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // 
   Y = x - t + p2;
 }
 FDFB_DEV u32 red8(u32 x, u32 p2, u32 p4) { return csub32(csub32(x, p4), p2); }   // [0, 8p) -> [0, 2p)
+FDFB_DEV u32 red16(u32 x, u32 p2) {                                                   // [0, 16p) -> [0, 2p)
+  return csub32(csub32(csub32(x, p2 << 2), p2 << 1), p2);
+}
 FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // GS, [0, 2p)
   const u32 x = X, y = Y;
   X = csub32(x + y + z, p2);                                            // [0, 2p)
@@ -116,10 +120,14 @@ FDFB_DEV void fwd8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
 #pragma unroll
     for (int k = 0; k < 4; k++) bfw32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2, z);
   }
+}
+// bound bookkeeping (in units of p): a radix-8 pass adds 6, the final pass 2 PLAST
+template <int V>
+FDFB_DEV void red16_all(u32 (&x)[V][8], u32 p2) {
 #pragma unroll
   for (int v = 0; v < V; v++)
 #pragma unroll
-    for (int k = 0; k < 8; k++) x[v][k] = red8(x[v][k], p2, p2 + p2);
+    for (int k = 0; k < 8; k++) x[v][k] = red16(x[v][k], p2);
 }
 template <int V>
 FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
@@ -227,17 +235,30 @@ FDFB_DEV void xstore(const u32 (&x)[V][8], u32* sb, int base, int S) {
   }
 }
 
-template <int N, int q, int V>
+template <int N, int q, int V, int BOUND>
 FDFB_DEV void fwd_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   if constexpr (q < BrShape<N>::NMID) {
     constexpr int T1 = N >> (3 * q + 3);
+    constexpr bool RED = BOUND + 6 > 16;              // this pass would leave [0, 16p): reduce first
+    constexpr int OUT = (RED ? 2 : BOUND) + 6;
     const int B = qbase<N, q>(tid);
     xload<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
+    if constexpr (RED) red16_all<V>(x, p2);
     fwd8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2, z);
     __syncwarp();
     xstore<N, q, V>(x, sb, lay_base<N, q>(B), T1);
     __syncwarp();
-    fwd_mid<N, q + 1, V>(x, sb, tid, tab, p, p2, z);
+    fwd_mid<N, q + 1, V, OUT>(x, sb, tid, tab, p, p2, z);
+  }
+}
+// bound (in p) of the values entering the final pass
+template <int N, int q, int BOUND>
+constexpr int fwd_bound_before_last() {
+  if constexpr (q < BrShape<N>::NMID) {
+    constexpr int OUT = ((BOUND + 6 > 16) ? 2 : BOUND) + 6;
+    return fwd_bound_before_last<N, q + 1, OUT>();
+  } else {
+    return BOUND;
   }
 }
 template <int N, int q, int V>
@@ -255,18 +276,28 @@ FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p,
 }
 
 // Forward NTT mod p of V polynomials. In: x[v][k] = coefficient tid + T k, [0, 2p).
-// Out: slot 8 tid + k, [0, 8p) (lazy last pass).  The caller guarantees that no thread still reads sb.
+// Out: slot 8 tid + k, [0, fwd_out_bound p) <= [0, 16p).  The caller guarantees that no
+// thread still reads sb.
 template <int N, int V>
 FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   using S = BrShape<N>;
   constexpr int T = S::T, NM = S::NMID;
-  fwd8_32<V>(x, tab, p, p2, z);
+  fwd8_32<V>(x, tab, p, p2, z);                       // inputs < 2p (digits < L <= p): bound 2 + 6
   xstore<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
   __syncthreads();
-  fwd_mid<N, 1, V>(x, sb, tid, tab, p, p2, z);
+  fwd_mid<N, 1, V, 8>(x, sb, tid, tab, p, p2, z);
   xload<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
+  constexpr int BL = fwd_bound_before_last<N, 1, 8>();
+  if constexpr (BL + 2 * S::PLAST > 16) red16_all<V>(x, p2);
   fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
 }
+// bound (in p) of the forward transform's outputs
+template <int N>
+constexpr int fwd_out_bound() {
+  constexpr int BL = fwd_bound_before_last<N, 1, 8>();
+  return ((BL + 2 * BrShape<N>::PLAST > 16) ? 2 : BL) + 2 * BrShape<N>::PLAST;
+}
+
 // Inverse NTT mod p (unscaled) of V polynomials. In: slot 8 tid + k, [0, 2p).  Out:
 // coefficient tid + T k, [0, 2p).  Starts warp-locally; ends after a CTA barrier.
 template <int N, int V>
@@ -383,9 +414,8 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
-                  const u32 xr = csub32(red8(x[v][k], pr2, pr2 + pr2), pr);   // [0, 8p) -> [0, p)
-                  mb[k] += (u64)xr * kb[k];                              // < 2 ell p^2 < 2^61
-                  ma[k] += (u64)xr * ka[k];
+                  mb[k] += (u64)x[v][k] * kb[k];      // x < 16p < 2^32, K < p < 2^28: < 2^60 each,
+                  ma[k] += (u64)x[v][k] * ka[k];      // 2 ell <= 8 terms < 2^63 (red64's range)
                 }
               }
             }
@@ -470,7 +500,7 @@ k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, 
   u32* o = dev + ((step * R.np + pi) * rows_per_step + r) * 2 * (size_t)N + (size_t)col * N + 8 * tid;
 #pragma unroll
   for (int k = 0; k < 8; k++) {
-    const u32 v = csub32(red8(x[0][k], pr2, pr2 + pr2), pr);
+    const u32 v = csub32(red16(x[0][k], pr2), pr);
     o[k] = csub32(shoup32(v, R.ninv[pi], R.ninvs[pi], pr), pr);
   }
 }
