@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fdfb", choices=["fdfb", "reference"])
     ap.add_argument("--config", default=None, help="configs/<name>.json (default: large / shift)")
-    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "shift"])
+    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "multilut", "tfhe", "shift", "permute"])
+    ap.add_argument("--luts", type=int, default=4, help="functions per input for --workload multilut")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="end-to-end steps (default: --steps)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -56,7 +57,7 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPU box); gloo only for functional tests")
     a = ap.parse_args()
     if a.config is None:
-        a.config = "shift" if a.workload == "shift" else "large"
+        a.config = "shift" if a.workload in ("shift", "permute") else "large"
     return a
 
 
@@ -366,6 +367,159 @@ class ShiftWorkload:
                 "d": "U[1, N-1] per ciphertext"}
 
 
+class MultiLutWorkload(BootstrapWorkload):
+    """fdfb_bootstrap_multi_batch: k LUTs on the same B inputs (ladder shared, PAPER.md:2568-2570);
+    the unit is one function evaluation (k per input)."""
+    metric = "functional bootstrap outputs/sec, k LUTs per input (N=2048)"
+    unit = "function evaluations/s"
+
+    def __init__(self, ctx, cfg, B, rank, world, dev, stream, k=4):
+        import torch
+        import synth
+        super().__init__(ctx, cfg, B, rank, world, dev, stream)
+        self.k = k
+        self.fs = [synth.lut(cfg, seed=1000 + i) for i in range(k)]
+        self.rotps = torch.stack([ctx.setup_lut(f) for f in self.fs])
+        from paper_2109_02731_b200.fdfb import lib
+        self.ws = ctx._bytes(lib().fdfb_workspace_bootstrap_multi(ctx.h, B, k))
+        self.ct_out = torch.empty((k, B, ctx.n + 1), dtype=torch.uint64, device=dev)
+        self.units = k
+        self.io_out_bytes = k * self.io_bytes
+
+    def step(self):
+        from paper_2109_02731_b200.fdfb import _check, _ptr, _stream, lib
+        c = self.ctx
+        _check(lib().fdfb_bootstrap_multi_batch(c.h, _ptr(self.keys["brk"]), _ptr(self.keys["bpk"]),
+                                                _ptr(self.keys["ksk"]), _ptr(self.rotps), self.k, _ptr(self.ct_in),
+                                                _ptr(self.ct_out), self.B, _ptr(self.ws), _stream(self.stream)))
+
+    def step_host(self, h_in, h_out):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.ct_in.copy_(h_in, non_blocking=True)
+            self.step()
+            h_out.copy_(self.ct_out, non_blocking=True)
+        self.stream.synchronize()
+
+    def host_buffers(self):
+        import torch
+        h_in = torch.empty(tuple(self.ct_in.shape), dtype=torch.uint64, pin_memory=True)
+        h_in.copy_(self.ct_in.cpu())
+        return h_in, torch.empty(tuple(self.ct_out.shape), dtype=torch.uint64, pin_memory=True)
+
+    def spot_check(self):
+        import numpy as np
+        cfg = self.cfg
+        s_h = self.keys["s"].cpu().numpy().astype(np.int64).astype(np.uint64)
+        q = 1 << cfg["log_q_lwe"]
+        ok = 0
+        for kk, f in enumerate(self.fs):
+            out_h = self.ct_out[kk, :16].cpu().numpy()
+            ph = (out_h[:, 0] - (out_h[:, 1:] * s_h[None, :]).sum(axis=1)) & np.uint64(q - 1)
+            dec = ((ph.astype(object) * cfg["t"] * 2 + q) // (2 * q)) % cfg["t"]
+            ok += sum(int(a) == int(b) for a, b in zip(dec, f[self.msgs[:16]]))
+        return {"lut_spot_check": "%d/%d outputs decrypt to f_k(m)" % (ok, 16 * self.k)}
+
+    def roofline(self, kernel_ms_per_step, ms_step):
+        per_cmux, _ = algorithmic_work(self.cfg)
+        n, u = self.cfg["n"], 2 if self.cfg["lwe_key"] == "ternary" else 1
+        modmul_step = per_cmux * n * u * self.B * (self.cfg["ell_boot"] + self.k)   # ell_boot + k rotations
+        imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
+        peak = 148 * IMAD_PER_SM_CLK * 1965e6
+        return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
+                "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None,
+                "blind_rotations_per_input": self.cfg["ell_boot"] + self.k}
+
+    def config(self):
+        d = super().config()
+        d["luts_per_input"] = self.k
+        return d
+
+
+class TfheWorkload(BootstrapWorkload):
+    """fdfb_bootstrap_tfhe_batch: the half-domain TFHE bootstrap (one blind rotation)."""
+    metric = "TFHE half-domain bootstraps/sec (N=2048)"
+    unit = "bootstraps/s"
+
+    def step(self):
+        self.ctx.bootstrap_tfhe(self.keys, self.rotp, self.ct_in, workspace=self.ws, stream=self.stream)
+
+    def step_host(self, h_in, h_out):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.ct_in.copy_(h_in, non_blocking=True)
+            out = self.ctx.bootstrap_tfhe(self.keys, self.rotp, self.ct_in, workspace=self.ws, stream=self.stream)
+            h_out.copy_(out, non_blocking=True)
+        self.stream.synchronize()
+        self.ct_out = out
+
+    def spot_check(self):
+        self.ct_out = self.ctx.bootstrap_tfhe(self.keys, self.rotp, self.ct_in, workspace=self.ws, stream=self.stream)
+        return {"note": "half-domain: correct for m < t/2 only (negacyclic); checked by the parity tests"}
+
+    def roofline(self, kernel_ms_per_step, ms_step):
+        per_cmux, _ = algorithmic_work(self.cfg)
+        n, u = self.cfg["n"], 2 if self.cfg["lwe_key"] == "ternary" else 1
+        modmul_step = per_cmux * n * u * self.B
+        imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
+        peak = 148 * IMAD_PER_SM_CLK * 1965e6
+        return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
+                "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None}
+
+
+class PermuteWorkload(ShiftWorkload):
+    """fdfb_permute over B RLWE ciphertexts with uniformly random permutations (Shift config keys)."""
+    metric = "permutes/sec (N=2048, L_pK=2, ell_pK=54)"
+    unit = "permutes/s"
+    kernel = "k_perm_bits + cuBLASLt int8 GEMM + k_permute_finish"
+
+    def __init__(self, ctx, cfg, B, rank, world, dev, stream):
+        import numpy as np
+        import torch
+        super().__init__(ctx, cfg, B, rank, world, dev, stream)
+        rng = np.random.default_rng(31 + rank)
+        self.perm = np.stack([rng.permutation(ctx.N) + 1 for _ in range(B)]).astype(np.uint32)
+        self.perm_dev = torch.from_numpy(self.perm).to(dev)
+        from paper_2109_02731_b200.fdfb import lib
+        self.ws = ctx._bytes(lib().fdfb_workspace_permute(ctx.h, B))
+
+    def step(self):
+        from paper_2109_02731_b200.fdfb import _check, _ptr, _stream, lib
+        c = self.ctx
+        _check(lib().fdfb_permute(c.h, _ptr(self.keys["pack"]), _ptr(self.ct_in), _ptr(self.perm_dev),
+                                  _ptr(self.ct_out), self.B, _ptr(self.ws), _stream(self.stream)))
+
+    def spot_check(self):
+        import numpy as np
+        self.d = np.zeros(self.B, np.int64)                     # reuse the phase check with a permutation
+        Q, N = self.cfg["Q"], self.cfg["N"]
+        Qu = np.uint64(Q)
+        S = self.keys["S"].cpu().numpy().astype(np.int64)
+        out = self.ct_out[:2].cpu().numpy()
+        worst = 0
+        for c in range(2):
+            ph = out[c, 0].copy()
+            a = out[c, 1]
+            for i in np.nonzero(S)[0]:
+                r = np.concatenate([(Qu - a[N - i:]) % Qu, a[:N - i]]) if i else a.copy()
+                if S[i] < 0:
+                    r = (Qu - r) % Qu
+                ph = np.where(ph >= r, ph - r, ph + Qu - r)
+            e = (ph + Qu - self.msg[c][self.perm[c] - 1]) % Qu
+            worst = max(worst, int(np.minimum(e, Qu - e).max()))
+        return {"permute_spot_check": "max |phase - m[pi]| over 2 outputs = 2^%.1f (Q = 2^%.1f)"
+                                      % (np.log2(max(worst, 1)), np.log2(Q))}
+
+    def roofline(self, kernel_ms_per_step, ms_step):
+        N, ell = self.cfg["N"], self.cfg["ell_pack"]
+        ops = 2.0 * (self.B * N) * (N * ell) * (14 * N)
+        tops = ops / (kernel_ms_per_step / 1e3) / 1e12
+        bf16 = json.load(open(PEAKS_FILE))["bf16_tflops"] if os.path.exists(PEAKS_FILE) else 1590.0
+        return {"kernel": self.kernel, "bound": "tensor", "achieved": tops, "peak": 2 * bf16,
+                "unit": "TOP/s (int8)", "frac": tops / (2 * bf16), "traffic": None,
+                "gemm": {"M": self.B * N, "K": N * ell, "N": 14 * N}}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -397,7 +551,11 @@ def main():
     B = args.batch or cfg["batch"]
     ctx = Context(cfg, local)
     stream = torch.cuda.current_stream()
-    W = (ShiftWorkload if args.workload == "shift" else BootstrapWorkload)(ctx, cfg, B, rank, world, dev, stream)
+    if args.workload == "multilut":
+        W = MultiLutWorkload(ctx, cfg, B, rank, world, dev, stream, k=args.luts)
+    else:
+        W = {"bootstrap": BootstrapWorkload, "tfhe": TfheWorkload, "shift": ShiftWorkload,
+             "permute": PermuteWorkload}[args.workload](ctx, cfg, B, rank, world, dev, stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MB > 126 MB L2
     torch.cuda.synchronize()
 
@@ -439,7 +597,7 @@ def main():
     if world > 1:
         ms = max_over_ranks(ms, device=dev)
     ms_step = ms / args.steps
-    value = B * world / (ms_step / 1e3)
+    value = B * world * getattr(W, "units", 1) / (ms_step / 1e3)
 
     # ------------------------------------------------------------------ end to end (host buffers)
     e2e_steps = args.e2e_steps or args.steps
@@ -460,7 +618,7 @@ def main():
         e_ms += a.elapsed_time(b)
     if world > 1:
         e_ms = max_over_ranks(e_ms, device=dev)
-    e2e_value = B * world / (e_ms / e2e_steps / 1e3)
+    e2e_value = B * world * getattr(W, "units", 1) / (e_ms / e2e_steps / 1e3)
     e2e_ok = bool(torch.equal(h_out, W.ct_out.cpu()))
 
     if rank == 0:
@@ -477,7 +635,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic", "config": cfgd, "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": W.unit, "steps": e2e_steps,
-                    "h2d_bytes_per_step": W.io_bytes, "d2h_bytes_per_step": W.io_bytes,
+                    "h2d_bytes_per_step": W.io_bytes, "d2h_bytes_per_step": getattr(W, "io_out_bytes", W.io_bytes),
                     "matches_device_path": e2e_ok},
             "roofline": roof, "clocks": clocks,
             "keygen_s": W.keygen_s, "key_broadcast_s": W.bcast_s,

@@ -18,11 +18,30 @@ def sources():
     return [os.path.join(d, f) for f in os.listdir(d)] + [os.path.join(os.path.dirname(HERE), "include", "fdfb.h")]
 
 
-def needs_build() -> bool:
-    if not os.path.exists(OUT):
+HASH = OUT + ".srchash"
+
+
+def source_hash() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for s in sorted(sources()):
+        if s.endswith((".cu", ".cuh", ".inc", ".h")):
+            h.update(os.path.basename(s).encode())
+            with open(s, "rb") as f:
+                h.update(f.read())
+    return h.hexdigest()
+
+
+def is_stale() -> bool:
+    """True if libfdfb.so was not built from the current sources (content hash, not mtimes)."""
+    if not os.path.exists(OUT) or not os.path.exists(HASH):
         return True
-    t = os.path.getmtime(OUT)
-    return any(os.path.getmtime(s) > t for s in sources())
+    with open(HASH) as f:
+        return f.read().strip() != source_hash()
+
+
+def needs_build() -> bool:
+    return is_stale()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -35,6 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode != 0:
             sys.stderr.write(r.stderr[-6000:])
             raise RuntimeError("nvcc failed (see %s)" % log)
+        with open(HASH, "w") as f:
+            f.write(source_hash())
         if verbose:
             sys.stderr.write(r.stderr)
     return OUT

@@ -53,6 +53,9 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise FdfbError("libfdfb.so not built (run __graft_entry__.build()); no CPU fallback exists")
+        from . import build as _build
+        if _build.is_stale():
+            raise FdfbError("libfdfb.so does not match its sources (stale build); run __graft_entry__.build()")
         L = C.CDLL(LIB_PATH)
         vp, u32, u64, sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_size_t
         L.fdfb_ctx_create.argtypes = [C.POINTER(fdfb_params), C.c_int, C.POINTER(vp)]
