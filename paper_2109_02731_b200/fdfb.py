@@ -51,11 +51,14 @@ def lib():
     """Load libfdfb.so (no fallback: raises if absent)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise FdfbError("libfdfb.so not built (run __graft_entry__.build()); no CPU fallback exists")
         from . import build as _build
-        if _build.is_stale():
-            raise FdfbError("libfdfb.so does not match its sources (stale build); run __graft_entry__.build()")
+        if _build.is_stale():                      # missing or built from other sources: rebuild (nvcc)
+            try:
+                _build.build()
+            except Exception as e:  # no nvcc / compile error: fail loudly, there is no CPU path
+                raise FdfbError("libfdfb.so missing or stale and the build failed: %s" % e)
+        if not os.path.exists(LIB_PATH) or _build.is_stale():
+            raise FdfbError("libfdfb.so not built (run __graft_entry__.build()); no CPU fallback exists")
         L = C.CDLL(LIB_PATH)
         vp, u32, u64, sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_size_t
         L.fdfb_ctx_create.argtypes = [C.POINTER(fdfb_params), C.c_int, C.POINTER(vp)]
