@@ -178,11 +178,8 @@ static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, 
                        const u32* abar, cudaStream_t st) {
   constexpr int T = N / 8;
   const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + exchange 2 planes 9N + Garner staging 16N bytes
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_blind_rotate<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr_set = true;
-  }
+  // function attributes are per device: set on every launch (host-side, ~µs), not once per process
+  cudaFuncSetAttribute(k_blind_rotate<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate<N, NP>, T, sm);
   if (per_sm < 1) per_sm = 1;
