@@ -669,6 +669,63 @@ void or_permute_batch(const u64* P, const u64* pack, const u64* ct, const uint32
     or_permute(P, pack, ct + (size_t)c * 2 * N, perm + (size_t)c * N, 0, out + (size_t)c * 2 * N);
 }
 
+/* ============================ Shift-based blind rotation / bootstrap (NEXT #4) ====
+ * BlindRotate_Shift(brK, acc, ct, u, pK) (Def. Shifting Based Blind
+ * Rotation): c = ModSwitch(ct, q, N) (done by the caller: abar in [0, N)); for i in [n],
+ * j in [u]:  acc <- CMux(brK[i,j], Shift(acc, -a[i] u[j] mod N), acc).
+ * Reading S1: Shift is defined for d in [N-1]; an amount of 0 is the
+ * identity, so that step is CMux(brK, acc, acc) = acc (exactly: Decomp(0) = 0).
+ * n_steps < n runs only the first n_steps LWE coefficients (timing samples). */
+void or_blind_rotate_shift(const u64* P, const u64* brk, const u64* pack, u64* acc, const uint32_t* abar,
+                           int n_steps) {
+  int N = (int)P[P_N], ell = (int)P[P_ELL_RGSW], logL = (int)P[P_LOGL_RGSW], u = u_len(P);
+  u64 Q = P[P_Q];
+  u64* g = (u64*)malloc(sizeof(u64) * 2 * N);
+  u64* out = (u64*)malloc(sizeof(u64) * 2 * N);
+  for (int i = 0; i < n_steps; i++)
+    for (int j = 0; j < u; j++) {
+      int64_t d = (-(int64_t)abar[i] * u_val(P, j)) % N;
+      if (d < 0) d += N;
+      if (d == 0) memcpy(g, acc, sizeof(u64) * 2 * N);             /* reading S1 */
+      else or_shift(P, pack, acc, (int)d, 0, g);
+      const u64* C = brk + ((size_t)i * u + j) * (size_t)2 * ell * 2 * N;
+      or_cmux(N, Q, logL, ell, C, g, acc, out);
+      memcpy(acc, out, sizeof(u64) * 2 * N);
+    }
+  free(g); free(out);
+}
+/* Shift-Based Bootstrapping:
+ *   1. rotP_b = Shift(rotP, b)        -- a plaintext cyclic shift: rotP_b[x] = rotP[(x - b) mod N]
+ *      (the message map of Shift), with b the mod-switched b~ = ModSwitch(b, q, N)
+ *      (reading S2: BlindRotate_Shift switches ct to Z_N in its step 1);
+ *   2. acc = [rotP_b, 0]               (reading S3: the "RLWE(s, 0)" is the trivial encryption,
+ *      as in the FDFB accumulator setup -- bootstrapping holds no secret key);
+ *   3. acc_BR = BlindRotate_Shift(brK, acc, ct, u, pK);
+ *   4-6. c_Q = SampleExt(acc_BR, 1); ModSwitch(Q -> q_lwe); KeySwitch mod q_lwe (order of c.3). */
+static void bootstrap_shift_one(const u64* P, const u64* brk, const u64* pack, const u64* ksk, const u64* rotp,
+                                const u64* ct, int n_steps, u64* out) {
+  int N = (int)P[P_N], n = (int)P[P_n], logq = (int)P[P_LOGQLWE]; u64 Q = P[P_Q];
+  u64 qlwe = 1ULL << logq;
+  uint32_t* abar = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t bbar = (uint32_t)or_mod_switch(ct[0], qlwe, (u64)N);
+  for (int i = 0; i < n; i++) abar[i] = (uint32_t)or_mod_switch(ct[1 + i], qlwe, (u64)N);
+  u64* acc = (u64*)calloc((size_t)2 * N, sizeof(u64));
+  for (int x = 0; x < N; x++) acc[x] = rotp[((x - (int)bbar) % N + N) % N];      /* steps 1-2 */
+  or_blind_rotate_shift(P, brk, pack, acc, abar, n_steps);                        /* step 3 */
+  u64* lwe = (u64*)malloc(sizeof(u64) * (N + 1));
+  or_sample_extract(N, Q, acc, 1, lwe);                                            /* step 4 */
+  for (int i = 0; i <= N; i++) lwe[i] = or_mod_switch(lwe[i], Q, qlwe);            /* step 5 */
+  or_keyswitch_lwe(P, ksk, lwe, out);                                              /* step 6 */
+  free(abar); free(acc); free(lwe);
+}
+void or_bootstrap_shift(const u64* P, const u64* brk, const u64* pack, const u64* ksk, const u64* rotp,
+                        const u64* ct_in, int count, int n_steps, u64* ct_out) {
+  int n = (int)P[P_n];
+  #pragma omp parallel for schedule(dynamic, 1) if (count > 1)
+  for (int c = 0; c < count; c++)
+    bootstrap_shift_one(P, brk, pack, ksk, rotp, ct_in + (size_t)c * (n + 1), n_steps, ct_out + (size_t)c * (n + 1));
+}
+
 /* RLWE encryption of a batch of message polynomials (Shift inputs), domain 8. */
 void or_rlwe_encrypt_batch(const u64* P, u64 seed, const int8_t* s, const u64* msgs, int count, u64* out) {
   int N = (int)P[P_N];

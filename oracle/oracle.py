@@ -252,6 +252,24 @@ class Oracle:
                                 C.c_int(cts.shape[0]), _p(out))
         return out
 
+    def blind_rotate_shift(self, brk, pk, acc, abar, n_steps=None):
+        """BlindRotate_Shift (reading S1); abar already in Z_N."""
+        acc = u64(acc).copy()
+        abar = np.ascontiguousarray(np.asarray(abar, dtype=np.uint32))
+        n_steps = self.n if n_steps is None else n_steps
+        lib().or_blind_rotate_shift(_p(self.P), _p(u64(brk)), _p(u64(pk)), _p(acc), _p(abar), C.c_int(n_steps))
+        return acc
+
+    def bootstrap_shift(self, keys, pk, rotp, cts, n_steps=None):
+        """Shift-based bootstrap (readings S1-S3, output order of c.3).
+        rotp: one plaintext polynomial (N coefficients in [0, Q))."""
+        cts = u64(cts).reshape(-1, self.n + 1)
+        out = np.zeros_like(cts)
+        n_steps = self.n if n_steps is None else n_steps
+        lib().or_bootstrap_shift(_p(self.P), _p(u64(keys["brk"])), _p(u64(pk)), _p(u64(keys["ksk"])),
+                                 _p(u64(rotp)), _p(cts), C.c_int(cts.shape[0]), C.c_int(n_steps), _p(out))
+        return out
+
     # ---------------------------------------------------------------- packing / shift
     def pack(self, pk, c, d):
         out = np.zeros((2, self.N), dtype=np.uint64)

@@ -550,3 +550,57 @@ def test_permute_lemma_and_reading(toy_pack):
         assert np.array_equal(o.rlwe_phase(S, out), msg[np.asarray(perm) - 1])
     bad = o.permute(pk, ct, perms[1], literal=True)
     assert not np.array_equal(o.rlwe_phase(S, bad), msg[perms[1] - 1])
+
+
+# ----------------------------------------------------------------------------- shift-based BR / bootstrap (NEXT #4)
+@pytest.mark.parametrize("lwe_key", ["binary", "ternary"])
+def test_blind_rotate_shift_message_law(lwe_key, toy_cfg):
+    """Lemma: BlindRotate_Shift leaves Shift(m_acc, -<a, s> mod N) -- a CYCLIC
+    rotation (no sign flips, unlike X^{-<a,s>}); zero mask coefficients exercise reading S1."""
+    cfg = dict(toy_cfg, lwe_key=lwe_key)
+    o = Oracle(cfg, noiseless=True)
+    K = o.keys(61)
+    pk = o.pack_key(62, K["S"])
+    N = o.N
+    rng = np.random.default_rng(63)
+    m = rng.integers(0, o.Q, N, dtype=np.uint64)
+    acc = np.zeros((2, N), np.uint64)
+    acc[0] = m
+    cases = [np.zeros(o.n, np.uint32), np.full(o.n, N - 1, np.uint32)]
+    cases += [rng.integers(0, N, o.n).astype(np.uint32) for _ in range(10)]
+    for abar in cases:
+        out = o.blind_rotate_shift(K["brk"], pk, acc, abar)
+        d = -sum(int(x) * int(y) for x, y in zip(abar, K["s"])) % N
+        assert np.array_equal(o.rlwe_phase(K["S"], out), np.roll(m, d)), abar
+    # the same accumulator through the negacyclic BR differs whenever a rotation wraps
+    abar = cases[-1]
+    assert not np.array_equal(o.rlwe_phase(K["S"], o.blind_rotate(K["brk"], acc, abar)),
+                              np.roll(m, -sum(int(x) * int(y) for x, y in zip(abar, K["s"])) % N))
+
+
+@pytest.mark.parametrize("lwe_key", ["binary", "ternary"])
+def test_bootstrap_shift_full_domain_noiseless(lwe_key, toy_cfg):
+    """Thm: out decrypts to (q/t) m_F with m_F = (t/Q) Coefs(Shift(rotP,
+    Phase(ct)))[1] = g((-y) mod N) for rotP[x] = Delta g(x), y the phase of ModSwitch(ct, q, N)
+    -- every residue of Z_N reachable, no negacyclic restriction (noiseless keys)."""
+    cfg = dict(toy_cfg, lwe_key=lwe_key)
+    o = Oracle(cfg, noiseless=True)
+    K = o.keys(71)
+    pk = o.pack_key(72, K["S"])
+    N, n, q, t = o.N, o.n, o.q_lwe, o.t
+    rng = np.random.default_rng(73)
+    g = rng.integers(0, t, N)
+    g[:2] = [t - 1, 1]
+    delta = (2 * o.Q + t) // (2 * t)
+    rotp = np.array([(delta * int(v)) % o.Q for v in g], np.uint64)
+    msgs = rng.integers(0, t, 3 * N).astype(np.uint64)
+    cts = o.lwe_encrypt(74, K["s"], msgs)
+    cts[:, 0] = (cts[:, 0] + rng.integers(0, q, len(cts)).astype(np.uint64)) % np.uint64(q)   # any phase
+    out = o.bootstrap_shift(K, pk, rotp, cts)
+    seen = set()
+    for c in range(len(cts)):
+        ms = [((2 * N * int(x) + q) // (2 * q)) % N for x in cts[c]]          # round(N x / q), ties up
+        y = (ms[0] - sum(a * int(s) for a, s in zip(ms[1:], K["s"]))) % N
+        seen.add(y)
+        assert o.decode(o.lwe_phase(K["s"], out[c]), q, t) == int(g[(-y) % N]), c
+    assert len(seen) > N // 2
