@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fdfb", choices=["fdfb", "reference"])
     ap.add_argument("--config", default=None, help="configs/<name>.json (default: large / shift)")
-    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "multilut", "tfhe", "shift", "permute"])
+    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "multilut", "tfhe", "shift", "permute",
+                                                                 "shiftboot"])
     ap.add_argument("--luts", type=int, default=4, help="functions per input for --workload multilut")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="end-to-end steps (default: --steps)")
@@ -57,7 +58,7 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPU box); gloo only for functional tests")
     a = ap.parse_args()
     if a.config is None:
-        a.config = "shift" if a.workload in ("shift", "permute") else "large"
+        a.config = "shift" if a.workload in ("shift", "permute", "shiftboot") else "large"
     return a
 
 
@@ -520,6 +521,102 @@ class PermuteWorkload(ShiftWorkload):
                 "gemm": {"M": self.B * N, "K": N * ell, "N": 14 * N}}
 
 
+class ShiftBootWorkload:
+    """fdfb_bootstrap_shift_batch: the shift-based bootstrap on the Shift
+    configuration -- n u = 2048 sequential steps, each one batched Shift (int8 GEMM over the
+    packing key) and one CMux per ciphertext; rotP = Delta g for a seeded g: Z_N -> Z_t."""
+    metric = "shift-based bootstraps/sec (N=2048, L_pK=2)"
+    unit = "bootstraps/s"
+    kclass = "shift_gemm"
+    kernel = "cuBLASLt int8 GEMM (Shift inside every CMux)"
+
+    def __init__(self, ctx, cfg, B, rank, world, dev, stream):
+        import numpy as np
+        import torch
+        import synth
+        from paper_2109_02731_b200.dist import broadcast_keys, shard_range
+        self.ctx, self.cfg, self.B, self.stream = ctx, cfg, B, stream
+        t0 = time.perf_counter()
+        if rank == 0:
+            keys = ctx.keygen(cfg["seeds"]["keys"], which=0x1B)
+        else:
+            keys = {"s": torch.empty(ctx.n, dtype=torch.int8, device=dev),
+                    "S": torch.empty(ctx.N, dtype=torch.int8, device=dev), "brk": ctx._bytes(ctx.sizes["brk"]),
+                    "bpk": None, "ksk": ctx._bytes(ctx.sizes["ksk"]), "pack": ctx._bytes(ctx.sizes["pack"])}
+        torch.cuda.synchronize()
+        self.keygen_s = time.perf_counter() - t0
+        self.bcast_s = 0.0
+        if world > 1:
+            t0 = time.perf_counter()
+            broadcast_keys(keys)
+            torch.cuda.synchronize()
+            self.bcast_s = time.perf_counter() - t0
+        self.keys = keys
+        N, t, Q = cfg["N"], cfg["t"], cfg["Q"]
+        rng = np.random.default_rng(cfg["seeds"]["lut"])
+        self.g = rng.integers(0, t, N)
+        delta = (2 * Q + t) // (2 * t)
+        self.rotp = torch.from_numpy(np.array([(delta * int(v)) % Q for v in self.g], np.uint64)).to(dev)
+        start, count = shard_range(B * world, world, rank)
+        self.msgs = synth.messages(cfg, B * world)[start:start + count]
+        self.ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"] + rank, keys["s"],
+                                     torch.from_numpy(self.msgs.copy()).to(dev))
+        self.ct_out = torch.empty_like(self.ct_in)
+        self.ws = ctx.workspace_bootstrap_shift(B)
+        self.io_bytes = B * (ctx.n + 1) * 8
+        self.key_bytes = ctx.sizes["brk"] + ctx.sizes["ksk"] + ctx.sizes["pack"]
+
+    def step(self):
+        self.ct_out = self.ctx.bootstrap_shift(self.keys, self.keys["pack"], self.rotp, self.ct_in,
+                                               workspace=self.ws, stream=self.stream)
+
+    def host_buffers(self):
+        import torch
+        h_in = torch.empty(tuple(self.ct_in.shape), dtype=torch.uint64, pin_memory=True)
+        h_in.copy_(self.ct_in.cpu())
+        return h_in, torch.empty_like(h_in).pin_memory()
+
+    def step_host(self, h_in, h_out):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.ct_in.copy_(h_in, non_blocking=True)
+            self.step()
+            h_out.copy_(self.ct_out, non_blocking=True)
+        self.stream.synchronize()
+
+    def spot_check(self):
+        """64 outputs decrypt to g((-y) mod N), y the phase of ModSwitch(ct, q, N) (plain numpy)."""
+        import numpy as np
+        cfg = self.cfg
+        N, t, q = cfg["N"], cfg["t"], 1 << cfg["log_q_lwe"]
+        s = self.keys["s"].cpu().numpy().astype(np.int64)
+        cin = self.ct_in[:64].cpu().numpy()
+        out = self.ct_out[:64].cpu().numpy()
+        ms = ((cin.astype(object) * 2 * N + q) // (2 * q)) % N
+        y = [(int(ms[c, 0]) - int(np.dot(ms[c, 1:].astype(np.int64), s))) % N for c in range(len(cin))]
+        ph = (out[:, 0] - (out[:, 1:] * s.astype(np.uint64)[None, :]).sum(axis=1)) & np.uint64(q - 1)
+        dec = ((ph.astype(object) * t * 2 + q) // (2 * q)) % t
+        ok = sum(int(d) == int(self.g[(-yy) % N]) for d, yy in zip(dec, y))
+        return {"lut_spot_check": "%d/%d outputs decrypt to g(-y mod N)" % (ok, len(cin))}
+
+    def roofline(self, kernel_ms_per_step, ms_step):
+        N, ell = self.cfg["N"], self.cfg["ell_pack"]
+        u = 2 if self.cfg["lwe_key"] == "ternary" else 1
+        K = ell * (N - 1) + N + ell * N
+        ops = 2.0 * (2 * self.B) * K * (7 * 2 * N) * self.cfg["n"] * u
+        tops = ops / (kernel_ms_per_step / 1e3) / 1e12
+        bf16 = json.load(open(PEAKS_FILE))["bf16_tflops"] if os.path.exists(PEAKS_FILE) else 1590.0
+        return {"kernel": self.kernel, "bound": "tensor", "achieved": tops, "peak": 2 * bf16,
+                "unit": "TOP/s (int8)", "frac": tops / (2 * bf16), "traffic": None,
+                "gemm": {"M": 2 * self.B, "K": K, "N": 7 * 2 * N, "per_step": self.cfg["n"] * u},
+                "peak_basis": "2 x MEASURED_PEAKS.json bf16_tflops (int8 = 2 x bf16 nominal)"}
+
+    def config(self):
+        cfg = self.cfg
+        return {"workload": cfg["name"] + "-shiftboot", "N": cfg["N"], "n": cfg["n"], "ell_pack": cfg["ell_pack"],
+                "L_pack": 1 << cfg["logL_pack"], "t": cfg["t"]}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -555,7 +652,7 @@ def main():
         W = MultiLutWorkload(ctx, cfg, B, rank, world, dev, stream, k=args.luts)
     else:
         W = {"bootstrap": BootstrapWorkload, "tfhe": TfheWorkload, "shift": ShiftWorkload,
-             "permute": PermuteWorkload}[args.workload](ctx, cfg, B, rank, world, dev, stream)
+             "permute": PermuteWorkload, "shiftboot": ShiftBootWorkload}[args.workload](ctx, cfg, B, rank, world, dev, stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MB > 126 MB L2
     torch.cuda.synchronize()
 

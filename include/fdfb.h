@@ -155,6 +155,20 @@ int fdfb_bootstrap_multi_batch(const fdfb_ctx* ctx, const void* brk, const void*
  * fdfb_workspace_bootstrap(ctx, B) bytes. */
 int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* ctx, const void* brk, const void* ksk, const uint64_t* rotp,
                               const uint64_t* ct_in, uint64_t* ct_out, uint32_t B, void* workspace, void* stream);
+/* Shift-based bootstrap (Def. PAPER.md:318-337 over BlindRotate_Shift PAPER.md:207-221,
+ * readings S1-S3, output order of c.3): ct_in [dev, B x (n+1)] mod q_lwe is switched to Z_N;
+ * acc = [Shift(rotP, b~), 0] with rotp [dev, N] ONE plaintext polynomial in [0, Q) (the
+ * cyclic rotation rotP[(x - b~) mod N]); for every (i, j): acc <- CMux(brK[i,j],
+ * Shift(acc, -a~_i u_j mod N), acc), the Shift evaluated homomorphically with the packing
+ * key `pack` (fdfb_keygen / fdfb_key_import FDFB_KEY_PACK; one int8 GEMM per step for
+ * L_pack = 2, else the streaming kernel); then SampleExt(., 1), ModSwitch Q -> q_lwe,
+ * KeySwitch -> ct_out [dev, B x (n+1)].  Evaluates ANY map Z_N -> Z_Q placed in rotP
+ * (full domain, no sign ladder); n u Shift evaluations per batch.  workspace [dev] of
+ * fdfb_workspace_bootstrap_shift(ctx, B) bytes. */
+size_t fdfb_workspace_bootstrap_shift(const fdfb_ctx* ctx, uint32_t B);
+int fdfb_bootstrap_shift_batch(const fdfb_ctx* ctx, const void* brk, const void* pack, const void* ksk,
+                               const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
+                               void* workspace, void* stream);
 /* Same, with ct_in/ct_out in (pinned) HOST memory: H2D copy, bootstrap, D2H copy,
  * all on `stream`; synchronises the stream before returning. */
 int fdfb_bootstrap_batch_host(const fdfb_ctx* ctx, const void* brk, const void* bpk, const void* ksk,

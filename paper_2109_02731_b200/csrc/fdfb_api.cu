@@ -173,34 +173,40 @@ static int launch_ntt_batch(const fdfb_ctx* c, u64* data, size_t count, int mode
   return FDFB_OK;
 }
 
-template <int N, int NP>
+template <int N, int NP, bool GIN>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
-                       const u32* abar, cudaStream_t st) {
+                       const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
   constexpr int T = N / 8;
   const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + exchange 2 planes 9N + Garner staging 16N bytes
   // function attributes are per device: set on every launch (host-side, ~µs), not once per process
-  cudaFuncSetAttribute(k_blind_rotate<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_blind_rotate<N, NP, GIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate<N, NP>, T, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate<N, NP, GIN>, T, sm);
   if (per_sm < 1) per_sm = 1;
   int grid = c->num_sms * per_sm;
   if (grid > n_acc) grid = n_acc;
   TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
-  k_blind_rotate<N, NP><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar);
+  k_blind_rotate<N, NP, GIN><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar,
+                                                   gin, s_begin);
   CKL(c);
   return FDFB_OK;
 }
 // blind-rotate n_acc accumulators; accumulator g uses mask row (g / acc_per_ct) % abar_rows
+// gin != nullptr: one shift-based step s_begin (k_blind_rotate GIN mode), else steps [0, n u)
 static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
-                     cudaStream_t st, int abar_rows = 0) {
+                     cudaStream_t st, int abar_rows = 0, const u64* gin = nullptr, int s_begin = 0) {
   if (n_acc <= 0) return FDFB_OK;
   if (abar_rows <= 0) abar_rows = (n_acc + acc_per_ct - 1) / acc_per_ct;
   const u32* k = (const u32*)bsk;
   const bool three = c->rns.np == 3;
-#define BR_CASE(NN)                                                                                  \
-  case NN:                                                                                           \
-    return three ? launch_br_t<NN, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st)            \
-                 : launch_br_t<NN, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st);
+  const int s0 = gin ? s_begin : 0;
+#define BR_CASE(NN)                                                                                          \
+  case NN:                                                                                                   \
+    if (gin)                                                                                                 \
+      return three ? launch_br_t<NN, 3, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st) \
+                   : launch_br_t<NN, 2, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st); \
+    return three ? launch_br_t<NN, 3, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st)  \
+                 : launch_br_t<NN, 2, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st);
   switch (c->prm.N) {
     BR_CASE(256)
     BR_CASE(512)
@@ -857,7 +863,7 @@ static int bootstrap_impl(const fdfb_ctx* c, const void* brk, const void* bpk, c
   size_t tot;
   // 1. ModSwitch(ct, q_lwe, 2N)
   tot = (size_t)B * (p.n + 1);
-  k_modswitch_in<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct_in, B, w.abar, w.bbar);
+  k_modswitch_in<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct_in, B, w.abar, w.bbar, (int)c->dp.logN + 1);
   CKL(c);
   // 2. ladder accumulators (reading R1)
   tot = (size_t)B * ellb * N;
@@ -935,7 +941,7 @@ extern "C" int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* c, const void* brk, con
   const int N = p.N;
   BootWs w = boot_ws(p, B, workspace);
   size_t tot = (size_t)B * (p.n + 1);
-  k_modswitch_in<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct_in, B, w.abar, w.bbar);
+  k_modswitch_in<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct_in, B, w.abar, w.bbar, (int)c->dp.logN + 1);
   CKL(c);
   tot = (size_t)B * N;
   k_tfhe_init<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rotp, w.bbar, (int)B, w.F);

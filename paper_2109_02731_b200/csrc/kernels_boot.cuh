@@ -6,10 +6,11 @@
 // ---------------------------------------------------------------------------
 // a1: ModSwitch(ct, q_lwe, 2N) -- round half up.
 // q_lwe = 2^w, 2N = 2^{logN+1}: round(2N x / q) = ((x >> (w - logN - 2)) + 1) >> 1.
+// logm: log2 of the target modulus (logN + 1 for 2N; logN for the shift-based BR's Z_N)
 __global__ void k_modswitch_in(DevParams p, const u64* __restrict__ ct, int B, u32* __restrict__ abar,
-                               u32* __restrict__ bbar) {
-  const int sh = p.log_q_lwe - (p.logN + 1) - 1;
-  const u32 m2N = 2 * p.N - 1;
+                               u32* __restrict__ bbar, int logm) {
+  const int sh = p.log_q_lwe - logm - 1;
+  const u32 m2N = (1u << logm) - 1;
   size_t total = (size_t)B * (p.n + 1);
   for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
     size_t c = x / (p.n + 1); int i = (int)(x % (p.n + 1));
@@ -248,4 +249,28 @@ __global__ void k_sample_extract(DevParams p, const u64* __restrict__ rlwe, cons
     }
     lwe[x] = v;
   }
+}
+
+// ------------------------------------------------------------------ shift-based bootstrap (NEXT #4)
+// Steps 1-2 of PAPER.md:322-323 (readings S2, S3): F[c] = [Shift(rotP, bbar_c), 0], the plaintext
+// cyclic rotation rotP_b[x] = rotP[(x - bbar_c) mod N], bbar in Z_N.
+__global__ void k_shiftboot_init(DevParams p, const u64* __restrict__ rotp, const u32* __restrict__ bbar, int B,
+                                 u64* __restrict__ F) {
+  const int N = p.N;
+  const size_t total = (size_t)B * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    const int cc = (int)(x / N), j = (int)(x % N);
+    F[(size_t)cc * 2 * N + j] = __ldg(rotp + ((j - (int)bbar[cc]) & (N - 1)));
+    F[(size_t)cc * 2 * N + N + j] = 0;
+  }
+}
+// Shift amount of step s = i u + j for every ciphertext: -abar_i u_j mod N, with 0 (the
+// identity, skipped by the CMux kernel, reading S1) replaced by a valid dummy 1.
+__global__ void k_shiftbr_amount(DevParams p, const u32* __restrict__ abar, int B, int s, u32* __restrict__ d) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  const int i = (p.u == 2) ? (s >> 1) : s, j = s - i * p.u;
+  const u32 a = abar[(size_t)c * p.n + i];
+  const u32 v = (p.u == 2 && j == 0) ? a : ((u32)p.N - a) & (u32)(p.N - 1);
+  d[c] = v ? v : 1u;
 }

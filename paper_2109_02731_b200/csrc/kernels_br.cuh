@@ -326,10 +326,15 @@ FDFB_DEV u64 shoup64_32(u32 c, u64 m, u64 ms, u64 Q) {
   return (u64)c * m - q * Q;
 }
 
-template <int N, int NP>
+// GIN = false: every step of the loop "for i in [n], j in [u]": CMux(brK[i,j], acc X^{-abar_i u_j}, acc).
+// GIN = true (shift-based BR): the rotated accumulator is given in gin
+// (Shift(acc, -abar_i u_j mod N), computed by the Shift GEMM); one step per launch; a zero
+// amount (abar_i = 0) is the identity step (reading S1) and is skipped.
+template <int N, int NP, bool GIN>
 __global__ void __launch_bounds__(N / 8, BrShape<N>::MINB)
 k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
-               int acc_per_ct, int abar_rows, const u32* __restrict__ abar) {
+               int acc_per_ct, int abar_rows, const u32* __restrict__ abar, const u64* __restrict__ gin,
+               int s_begin) {
   using S = BrShape<N>;
   constexpr int T = S::T;
   extern __shared__ u64 smem[];
@@ -351,11 +356,17 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
     for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
     const u32* ab = abar + (size_t)((g / acc_per_ct) % abar_rows) * p.n;   // accumulator g uses abar row
+    // GIN: the single step s_begin = i0 u + j0; otherwise every (i, j)
+    const int i0 = GIN ? s_begin / u : 0, i1 = GIN ? i0 + 1 : p.n;
+    const int j0 = GIN ? s_begin - i0 * u : 0, j1 = GIN ? j0 + 1 : u;
 #pragma unroll 1
-    for (int i = 0; i < p.n; i++) {
+    for (int i = i0; i < i1; i++) {
       const u32 ai = __ldg(ab + i);
+      if constexpr (GIN) {
+        if (ai == 0) continue;                     // Shift(acc, 0) = acc: CMux(brK, acc, acc) = acc
+      }
 #pragma unroll 1
-      for (int j = 0; j < u; j++) {
+      for (int j = j0; j < j1; j++) {
         // exponent -abar_i u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
@@ -373,13 +384,22 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
             __syncthreads();                       // acc writes (previous step) / sb readers done
             // d = acc X^e - acc of this half (thread-private slots of sd; branchless rotation)
             const u64* src = sacc + half * N;
+            if constexpr (GIN) {
+              const u64* gsrc = gin + (size_t)g * 2 * N + half * N;
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-              const int pos = tid + T * k;
-              const int idx = (pos - e) & (2 * N - 1);     // coefficient pos of X^e a = +-a[idx mod N]
-              const u64 v = src[idx & (N - 1)];
-              const u64 rv = (idx >= N && v) ? Q - v : v;
-              sd[pos] = sub_mod(rv, src[pos], Q);
+              for (int k = 0; k < 8; k++) {
+                const int pos = tid + T * k;
+                sd[pos] = sub_mod(__ldg(gsrc + pos), src[pos], Q);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 8; k++) {
+                const int pos = tid + T * k;
+                const int idx = (pos - e) & (2 * N - 1);     // coefficient pos of X^e a = +-a[idx mod N]
+                const u64 v = src[idx & (N - 1)];
+                const u64 rv = (idx >= N && v) ? Q - v : v;
+                sd[pos] = sub_mod(rv, src[pos], Q);
+              }
             }
             // digit pairs (r, r+1) transformed together; an odd ell pairs the last digit with zero
 #pragma unroll 1

@@ -43,7 +43,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_status_string", "fdfb_last_cuda_error", "fdfb_timing_enable", "fdfb_timing_read",
             "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming",
             "fdfb_workspace_keyswitch", "fdfb_workspace_bootstrap_multi", "fdfb_bootstrap_multi_batch",
-            "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute"]
+            "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute",
+            "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -86,6 +87,9 @@ def lib():
         L.fdfb_workspace_bootstrap_multi.restype = sz
         L.fdfb_bootstrap_multi_batch.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp, u32, vp, vp]
         L.fdfb_bootstrap_tfhe_batch.argtypes = [vp, vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_workspace_bootstrap_shift.argtypes = [vp, u32]
+        L.fdfb_workspace_bootstrap_shift.restype = sz
+        L.fdfb_bootstrap_shift_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_workspace_permute.argtypes = [vp, u32]
         L.fdfb_workspace_permute.restype = sz
         L.fdfb_permute.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
@@ -277,6 +281,18 @@ class Context:
         ws = self.workspace_bootstrap(B) if workspace is None else workspace
         _check(lib().fdfb_bootstrap_tfhe_batch(self.h, _ptr(keys["brk"]), _ptr(keys["ksk"]), _ptr(rotp), _ptr(ct_in),
                                                _ptr(out), B, _ptr(ws), _stream(stream)))
+        return out
+
+    def workspace_bootstrap_shift(self, B):
+        return self._bytes(lib().fdfb_workspace_bootstrap_shift(self.h, B))
+
+    def bootstrap_shift(self, keys, pack, rotp, ct_in, workspace=None, stream=None):
+        """Shift-based bootstrap: rotp is ONE plaintext polynomial [N] in [0, Q)."""
+        B = ct_in.shape[0]
+        out = self._u64(B, self.n + 1)
+        ws = self.workspace_bootstrap_shift(B) if workspace is None else workspace
+        _check(lib().fdfb_bootstrap_shift_batch(self.h, _ptr(keys["brk"]), _ptr(pack), _ptr(keys["ksk"]), _ptr(rotp),
+                                                _ptr(ct_in), _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
 
     def bootstrap_batch_host(self, keys, rotp, ct_in_host, ct_out_host, workspace, stream=None):

@@ -469,3 +469,69 @@ def test_bootstrap_host_buffers_api():
     h_out = torch.empty_like(h_in).pin_memory()
     ctx.bootstrap_batch_host(dk, rot, h_in, h_out, ctx.workspace_bootstrap(9))
     assert np.array_equal(h_out.numpy(), H(ctx.bootstrap_batch(dk, rot, T(cts))))
+
+
+# ----------------------------------------------------------------------------- shift-based bootstrap (NEXT #4)
+SHIFTBOOT256 = {  # shift-based bootstrap on the int8-GEMM Shift path (L_pK = 2), ternary u, small n
+    "name": "shiftboot256", "N": 256, "n": 16, "Q": 134215681, "log_q_lwe": 32, "lwe_key": "ternary",
+    "rlwe_key": "ternary", "logL_rgsw": 9, "ell_rgsw": 3, "logL_boot": 9, "ell_boot": 3, "logL_pk": 9,
+    "ell_pk": 3, "logL_ks": 4, "ell_ks": 8, "logL_pack": 1, "ell_pack": 27, "t": 16, "sigma": 3.2,
+    "batch": 5, "seeds": {"keys": 9101, "msgs": 9102, "lut": 9103, "err": 9104}}
+
+
+def _shiftboot_inputs(cfg, orc, s, B, seed):
+    """Random-phase LWE inputs (a few with zero mask coefficients: the identity steps of
+    reading S1) and a random plaintext rotP = Delta g, g: Z_N -> Z_t."""
+    rng = np.random.default_rng(seed)
+    N, q, t, Q = cfg["N"], 1 << cfg["log_q_lwe"], cfg["t"], cfg["Q"]
+    cts = orc.lwe_encrypt(seed, s, rng.integers(0, t, B).astype(np.uint64))
+    cts[:, 0] = (cts[:, 0] + rng.integers(0, q, B, dtype=np.uint64)) % np.uint64(q)
+    cts[0, 1:5] = 0
+    if B > 1:
+        cts[1, 1:] = np.uint64(q // N) * np.uint64(N - 1)        # every a~_i = N - 1
+    g = rng.integers(0, t, N)
+    delta = (2 * Q + t) // (2 * t)
+    rotp = np.array([(delta * int(v)) % Q for v in g], np.uint64)
+    return cts, g, rotp
+
+
+@pytest.mark.parametrize("name,B", [("tiny_shift", 3), ("shiftboot256", 5)])
+def test_bootstrap_shift_bit_exact(name, B):
+    """Shift-based bootstrap bit-exact with the oracle: the streaming Shift
+    (L_pK = 512, binary u) and the int8-GEMM Shift (L_pK = 2, ternary u, ragged batch)."""
+    cfg = SHIFTBOOT256 if name == "shiftboot256" else synth.load_config(name)
+    orc = Oracle(cfg)
+    K = orc.keys(cfg["seeds"]["keys"])
+    pk = orc.pack_key(cfg["seeds"]["keys"], K["S"])
+    ctx = Context(cfg, 0)
+    dk = {"brk": ctx.key_import(KEY_BRK, T(K["brk"].reshape(-1))),
+          "ksk": ctx.key_import(KEY_KSK, T(K["ksk"].reshape(-1)))}
+    dpk = ctx.key_import(KEY_PACK, T(pk.reshape(-1)))
+    cts, g, rotp = _shiftboot_inputs(cfg, orc, K["s"], B, seed=31)
+    got = H(ctx.bootstrap_shift(dk, dpk, T(rotp), T(cts)))
+    ctx.device_status()
+    assert np.array_equal(got, orc.bootstrap_shift(K, pk, rotp, cts))
+
+
+@pytest.mark.slow
+def test_bootstrap_shift_large_noisy_full_domain():
+    """Shift configuration (N = 2048, n = 1024 ternary, L_pK = 2, sigma = 3.2 keys from the GPU
+    keygen): every output decrypts to g((-y) mod N), y the phase of ModSwitch(ct, q, N) -- the
+    full Z_N domain with no negacyclic restriction (Thm)."""
+    cfg = synth.load_config("shift")
+    ctx = Context(cfg, 0)
+    keys = ctx.keygen(cfg["seeds"]["keys"], which=0x1B)        # s, S, brK, ksK, pack
+    orc = Oracle(cfg)
+    s = H(keys["s"])
+    B = 24
+    cts_h, g, rotp = _shiftboot_inputs(cfg, orc, s, B, seed=41)
+    out = H(ctx.bootstrap_shift(keys, keys["pack"], T(rotp), T(cts_h)))
+    ctx.device_status()
+    N, t, q = cfg["N"], cfg["t"], 1 << cfg["log_q_lwe"]
+    s64 = s.astype(np.int64)
+    ms = ((cts_h.astype(object) * 2 * N + q) // (2 * q)) % N              # ModSwitch(ct, q, N)
+    y = [(int(ms[c, 0]) - int(np.dot(ms[c, 1:].astype(np.int64), s64))) % N for c in range(B)]
+    su = s64.astype(np.uint64)
+    ph = (out[:, 0] - (out[:, 1:] * su[None, :]).sum(axis=1)) & np.uint64(q - 1)
+    dec = [int(x) for x in ((ph.astype(object) * t * 2 + q) // (2 * q)) % t]
+    assert dec == [int(g[(-yy) % N]) for yy in y]
