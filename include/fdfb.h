@@ -14,6 +14,8 @@
  *     validated before any launch, so an error return means nothing ran,
  *     except FDFB_E_CUDA (a launch or runtime call failed; see
  *     fdfb_last_cuda_error).  Nothing throws across the ABI.
+ *   - A batch count of 0 (B, count) returns FDFB_OK before any other check except
+ *     the context: its data pointers may then be NULL (empty tensors).
  *   - Ciphertext layouts (canonical, coefficient domain, residues canonical):
  *       LWE  [b, a_1..a_n] as uint64, mod q_lwe = 2^log_q_lwe (inputs/outputs
  *            of bootstrap/keyswitch) or mod Q (SampleExt outputs, VectorPack

@@ -677,8 +677,9 @@ extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int
 extern "C" int fdfb_keygen_canonical(const fdfb_ctx* c, uint64_t seed, int kind, const int8_t* sk_lwe,
                                      const int8_t* sk_rlwe, const uint64_t* idx, uint32_t count, uint64_t* out,
                                      void* stream) {
-  if (!c || !idx || !out || !sk_lwe || !sk_rlwe) return FDFB_E_NULL;
-  if (count == 0) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (count == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!idx || !out || !sk_lwe || !sk_rlwe) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   const int N = c->prm.N;
   u64* didx = nullptr;
@@ -751,8 +752,9 @@ extern "C" int fdfb_key_export(const fdfb_ctx* c, int kind, const void* dev_key,
 
 extern "C" int fdfb_lwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_lwe, const uint64_t* msg,
                                 uint32_t count, uint32_t flags, uint64_t* out, void* stream) {
-  if (!c || !sk_lwe || !msg || !out) return FDFB_E_NULL;
-  if (!count) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!sk_lwe || !msg || !out) return FDFB_E_NULL;
   k_lwe_encrypt<<<((size_t)count * 32 + 255) / 256, 256, 0, S(stream)>>>(c->dp, seed, sk_lwe, msg, count, flags, out);
   CKL(c);
   return FDFB_OK;
@@ -760,8 +762,9 @@ extern "C" int fdfb_lwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* 
 
 extern "C" int fdfb_rlwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_rlwe, const uint64_t* msg,
                                  uint32_t count, uint64_t* out, void* stream) {
-  if (!c || !sk_rlwe || !msg || !out) return FDFB_E_NULL;
-  if (!count) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!sk_rlwe || !msg || !out) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   const int N = c->prm.N;
   u64 *shat, *tm, *tp;
@@ -818,7 +821,9 @@ extern "C" int fdfb_setup_lut(const fdfb_ctx* c, const uint64_t* lut, uint32_t t
 // ------------------------------------------------------------------ hot path
 extern "C" int fdfb_blind_rotate(const fdfb_ctx* c, const void* brk, uint64_t* acc, const uint32_t* abar,
                                  uint32_t count, uint32_t acc_per_ct, void* stream) {
-  if (!c || !brk || !acc || !abar) return FDFB_E_NULL;
+  if (!c) return FDFB_E_NULL;
+  if (count == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!brk || !acc || !abar) return FDFB_E_NULL;
   if (acc_per_ct == 0) return FDFB_E_DIMENSION;
   return launch_br(c, (const u64*)brk, acc, (int)count, (int)acc_per_ct, abar, S(stream));
 }
@@ -905,17 +910,19 @@ static int bootstrap_impl(const fdfb_ctx* c, const void* brk, const void* bpk, c
 extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
                                     const uint64_t* rotp, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B,
                                     void* workspace, void* stream) {
-  if (!c || !brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
-  if (B == 0) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
   return bootstrap_impl(c, brk, bpk, ksk, rotp, 1, ct_in, ct_out, B, workspace, S(stream));
 }
 
 extern "C" int fdfb_bootstrap_multi_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
                                           const uint64_t* rotp, uint32_t k, const uint64_t* ct_in, uint64_t* ct_out,
                                           uint32_t B, void* workspace, void* stream) {
-  if (!c || !brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
+  if (!c) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
   if (k == 0) return FDFB_E_DIMENSION;
-  if (B == 0) return FDFB_OK;
   return bootstrap_impl(c, brk, bpk, ksk, rotp, k, ct_in, ct_out, B, workspace, S(stream));
 }
 
@@ -934,8 +941,9 @@ __global__ void k_tfhe_init(DevParams p, const u64* __restrict__ rotp0, const u3
 extern "C" int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* c, const void* brk, const void* ksk, const uint64_t* rotp,
                                          const uint64_t* ct_in, uint64_t* ct_out, uint32_t B, void* workspace,
                                          void* stream) {
-  if (!c || !brk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
-  if (B == 0) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!brk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   const fdfb_params& p = c->prm;
   const int N = p.N;
@@ -957,8 +965,9 @@ extern "C" int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* c, const void* brk, con
 extern "C" int fdfb_bootstrap_batch_host(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,
                                          const uint64_t* rotp, const uint64_t* in_h, uint64_t* out_h, uint32_t B,
                                          void* workspace, void* stream) {
-  if (!c || !in_h || !out_h || !workspace) return FDFB_E_NULL;
-  if (B == 0) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!in_h || !out_h || !workspace) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   size_t bytes = (size_t)B * (c->prm.n + 1) * 8;
   BootWs w = boot_ws(c->prm, B, workspace);
@@ -974,8 +983,9 @@ extern "C" int fdfb_bootstrap_batch_host(const fdfb_ctx* c, const void* brk, con
 
 extern "C" int fdfb_sample_extract(const fdfb_ctx* c, const uint64_t* rlwe, const uint32_t* k, uint64_t* lwe,
                                    uint32_t B, void* stream) {
-  if (!c || !rlwe || !k || !lwe) return FDFB_E_NULL;
-  if (!B) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (!B) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!rlwe || !k || !lwe) return FDFB_E_NULL;
   size_t tot = (size_t)B * (c->prm.N + 1);
   k_sample_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, S(stream)>>>(c->dp, rlwe, k, B, lwe, c->d_status);
   CKL(c);
@@ -987,15 +997,17 @@ extern "C" size_t fdfb_workspace_keyswitch(const fdfb_ctx* c, uint32_t B) {
 }
 extern "C" int fdfb_lwe_keyswitch(const fdfb_ctx* c, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
                                   uint32_t B, void* workspace, void* stream) {
-  if (!c || !ksk || !lwe_N || !lwe_n) return FDFB_E_NULL;
-  if (!B) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (!B) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!ksk || !lwe_N || !lwe_n) return FDFB_E_NULL;
   return keyswitch_lwe(c, (const u64*)ksk, lwe_N, (int)B, lwe_n, workspace, S(stream));
 }
 
 extern "C" int fdfb_poly_mul(const fdfb_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
                              void* stream) {
-  if (!c || !a || !b || !out) return FDFB_E_NULL;
-  if (!count) return FDFB_OK;
+  if (!c) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!a || !b || !out) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   const int N = c->prm.N;
   u64* tb;

@@ -535,3 +535,31 @@ def test_bootstrap_shift_large_noisy_full_domain():
     ph = (out[:, 0] - (out[:, 1:] * su[None, :]).sum(axis=1)) & np.uint64(q - 1)
     dec = [int(x) for x in ((ph.astype(object) * t * 2 + q) // (2 * q)) % t]
     assert dec == [int(g[(-yy) % N]) for yy in y]
+
+
+# ----------------------------------------------------------------------------- empty batches
+def test_empty_batches_are_noops():
+    """B = 0 (empty tensors, NULL data pointers) is FDFB_OK and launches nothing on every batched
+    entry point (include/fdfb.h conventions)."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    rot = ctx.setup_lut(synth.lut(cfg))
+    e_lwe = torch.empty((0, cfg["n"] + 1), dtype=torch.uint64, device=DEV)
+    e_rlwe = torch.empty((0, 2, cfg["N"]), dtype=torch.uint64, device=DEV)
+    e_u32 = torch.empty(0, dtype=torch.uint32, device=DEV)
+    torch.cuda.synchronize()
+    n0 = ctx.launch_count()
+    assert ctx.bootstrap_batch(dk, rot, e_lwe).shape == (0, cfg["n"] + 1)
+    assert ctx.bootstrap_tfhe(dk, rot, e_lwe).shape[0] == 0
+    assert ctx.bootstrap_multi(dk, torch.stack([rot, rot]), e_lwe).numel() == 0
+    assert ctx.sample_extract(e_rlwe, e_u32).shape[0] == 0
+    ctx.blind_rotate(dk["brk"], e_rlwe, e_u32)
+    torch.cuda.synchronize()
+    assert ctx.launch_count() == n0
+    pcfg, porc, s, S, pk, pctx, dpk = pack_setup("tiny_shift")
+    e_rlwe2 = torch.empty((0, 2, pcfg["N"]), dtype=torch.uint64, device=DEV)
+    n1 = pctx.launch_count()
+    assert pctx.shift(dpk, e_rlwe2, e_u32).shape[0] == 0
+    assert pctx.permute(dpk, e_rlwe2, torch.empty((0, pcfg["N"]), dtype=torch.uint32, device=DEV)).shape[0] == 0
+    torch.cuda.synchronize()
+    assert pctx.launch_count() == n1
+    pctx.device_status()
