@@ -177,7 +177,7 @@ template <int N, int NP, bool GIN>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
                        const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
   constexpr int T = N / 8;
-  const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 8N + exchange 2 planes 9N + Garner staging 16N bytes
+  const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 16N + exchange 2 planes 9N + CRT sums 8N bytes
   // function attributes are per device: set on every launch (host-side, ~µs), not once per process
   cudaFuncSetAttribute(k_blind_rotate<N, NP, GIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int per_sm = 0;
@@ -402,9 +402,10 @@ static int setup_rns(fdfb_ctx* c) {
     if (cand >= (1ULL << 28) || cand == p.Q || !h_is_prime(cand)) continue;
     primes.push_back(cand);
     P *= cand;
-    if (primes.size() >= 2 && P / 2 > bound + 1) break;
+    if (primes.size() >= 2 && P / 8 * 3 > bound + 1) break;
   }
-  if (primes.size() < 2 || P / 2 <= bound + 1) return FDFB_E_UNSUPPORTED;
+  // |V| <= bound < 3P/8 keeps sum_i t_i / p_i within 1/8 of an integer (the kernel's CRT rounding)
+  if (primes.size() < 2 || P / 8 * 3 <= bound + 1) return FDFB_E_UNSUPPORTED;
   R.np = (int)primes.size();
   const u64 Q = p.Q;
   std::vector<u32> ft, it;
@@ -425,15 +426,18 @@ static int setup_rns(fdfb_ctx* c) {
     }
   }
   auto s32 = [](u64 w, u64 m) { return (u32)((w << 32) / m); };
-  R.g01 = (u32)h_inv(primes[0], primes[1]); R.g01s = s32(R.g01, primes[1]);
-  if (R.np == 3) {
-    R.g02 = (u32)h_inv(h_mulmod(primes[0], primes[1], primes[2]), primes[2]); R.g02s = s32(R.g02, primes[2]);
-    R.g12 = (u32)h_inv(primes[1], primes[2]); R.g12s = s32(R.g12, primes[2]);
+  for (int i = 0; i < R.np; i++) {                 // CRT constants (kernels_br.cuh epilogue)
+    u64 Pi_q = 1 % Q, Pi_p = 1;                    // P / p_i mod Q and mod p_i
+    for (int j = 0; j < R.np; j++) {
+      if (j == i) continue;
+      Pi_q = h_mulmod(Pi_q, primes[j] % Q, Q);
+      Pi_p = h_mulmod(Pi_p, primes[j] % primes[i], primes[i]);
+    }
+    R.y[i] = (u32)h_inv(Pi_p, primes[i]); R.ys[i] = s32(R.y[i], primes[i]);
+    R.M[i] = Pi_q; R.Ms[i] = shoup_of(Pi_q, Q);
+    R.fs[i] = (float)(32.0 / (double)primes[i]);
   }
-  R.m0 = 1 % Q; R.m0s = shoup_of(R.m0, Q);
-  R.m1 = primes[0] % Q; R.m1s = shoup_of(R.m1, Q);
-  R.m2 = R.np == 3 ? h_mulmod(primes[0] % Q, primes[1] % Q, Q) : 0; R.m2s = shoup_of(R.m2, Q);
-  R.pmq = (u64)(P % Q);
+  R.pq = (u64)(P % Q);
   ft.insert(ft.end(), it.begin(), it.end());
   CK(cudaMalloc(&c->d_rtab, ft.size() * 4));
   CK(cudaMemcpy(c->d_rtab, ft.data(), ft.size() * 4, cudaMemcpyHostToDevice));

@@ -52,10 +52,11 @@ struct RnsParams {
   u32 r32[RNS_MAXP], r32s[RNS_MAXP];      // 2^32 mod p and its Shoup companion
   u32 b32[RNS_MAXP];                      // floor(2^32 / p)  (reduction of a 32-bit word)
   u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} mod p (key import)
-  // Garner: c1 = (r1 - c0) g01 mod p1;  c2 = (r2 - c0) g02 - c1 g12 mod p2
-  u32 g01, g01s, g02, g02s, g12, g12s;
-  u64 m0, m0s, m1, m1s, m2, m2s;          // 1, p0, p0 p1 mod Q (+ 64-bit Shoup companions)
-  u64 pmq;                                // P mod Q (sign correction)
+  // CRT: t_i = r_i y_i mod p_i with y_i = (P/p_i)^{-1} mod p_i;  V = sum t_i M_i - k P
+  u32 y[RNS_MAXP], ys[RNS_MAXP];          // y_i and its Shoup companion
+  u64 M[RNS_MAXP], Ms[RNS_MAXP];          // (P/p_i) mod Q and its 64-bit Shoup companion
+  u64 pq;                                 // P mod Q
+  float fs[RNS_MAXP];                     // 32 / p_i  (t_i / p_i from the top 23 bits of t_i)
   u32 zero;                               // 0, opaque to the compiler (see bfw32)
   const uint4* ftab;                      // [np][GROUPS][8 pairs] forward (w, w') u32
   const uint4* itab;                      // inverse
@@ -339,10 +340,9 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
   constexpr int T = S::T;
   extern __shared__ u64 smem[];
   u64* sacc = smem;                          // [b | a], natural order, canonical mod Q
-  u64* sd = smem + 2 * N;                    // d = acc X^e - acc of one half (thread-private slots)
-  u32* sb = (u32*)(smem + 3 * N);            // NTT exchange buffer: 2 planes of 9N/8 words
-  u32* st0 = sb + 2 * Lay<N>::WORDS;         // Garner staging: c0 [2][N]
-  u32* st1 = st0 + 2 * N;                    //                 c1 [2][N]
+  u64* sd = smem + 2 * N;                    // d = acc X^e - acc, both halves (thread-private slots)
+  u32* sb = (u32*)(smem + 4 * N);            // NTT exchange buffer: 2 planes of 9N/8 words
+  float* sfr = (float*)(sb + 2 * Lay<N>::WORDS);   // CRT: running sum of t_i / p_i per output [2][N]
   const int tid = threadIdx.x;
   const u64 Q = p.Q;
   const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
@@ -370,6 +370,30 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
         // exponent -abar_i u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
+        __syncthreads();                           // acc of the previous step complete
+        // d = acc X^e - acc for both halves, once per CMux (thread-private slots of sd; the
+        // epilogues below may then update acc prime by prime)
+        if constexpr (GIN) {
+          const u64* gsrc = gin + (size_t)g * 2 * N;
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            const int pos = tid + T * k;
+            sd[pos] = sub_mod(__ldg(gsrc + pos), sacc[pos], Q);
+          }
+        } else {
+#pragma unroll
+          for (int half = 0; half < 2; half++) {
+            const u64* src = sacc + half * N;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              const int pos = tid + T * k;
+              const int idx = (pos - e) & (2 * N - 1);     // coefficient pos of X^e a = +-a[idx mod N]
+              const u64 v = src[idx & (N - 1)];
+              const u64 rv = (idx >= N && v) ? Q - v : v;
+              sd[half * N + pos] = sub_mod(rv, src[pos], Q);
+            }
+          }
+        }
 #pragma unroll 1
         for (int pi = 0; pi < NP; pi++) {
           const u32 pr = R.p[pi], pr2 = R.p2[pi];
@@ -381,26 +405,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
 #pragma unroll 1
           for (int half = 0; half < 2; half++) {
-            __syncthreads();                       // acc writes (previous step) / sb readers done
-            // d = acc X^e - acc of this half (thread-private slots of sd; branchless rotation)
-            const u64* src = sacc + half * N;
-            if constexpr (GIN) {
-              const u64* gsrc = gin + (size_t)g * 2 * N + half * N;
-#pragma unroll
-              for (int k = 0; k < 8; k++) {
-                const int pos = tid + T * k;
-                sd[pos] = sub_mod(__ldg(gsrc + pos), src[pos], Q);
-              }
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; k++) {
-                const int pos = tid + T * k;
-                const int idx = (pos - e) & (2 * N - 1);     // coefficient pos of X^e a = +-a[idx mod N]
-                const u64 v = src[idx & (N - 1)];
-                const u64 rv = (idx >= N && v) ? Q - v : v;
-                sd[pos] = sub_mod(rv, src[pos], Q);
-              }
-            }
+            const u64* sdh = sd + half * N;
             // digit pairs (r, r+1) transformed together; an odd ell pairs the last digit with zero
 #pragma unroll 1
             for (int r = 0; r < ell; r += 2) {
@@ -417,11 +422,11 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
               const int sh = r * logL;
 #pragma unroll
               for (int k = 0; k < 8; k++) {
-                const u64 dv = sd[tid + T * k];
+                const u64 dv = sdh[tid + T * k];
                 x[0][k] = (u32)(dv >> sh) & dmask;
                 x[1][k] = two ? (u32)(dv >> (sh + logL)) & dmask : 0u;
               }
-              if (r > 0) __syncthreads();          // previous pair's readers of sb done
+              if (pi > 0 || half > 0 || r > 0) __syncthreads();   // previous readers of sb done
               ntt_fwd32<N, 2>(x, sb, tid, ft, pr, pr2, R.zero);
 #pragma unroll
               for (int v = 0; v < 2; v++) {
@@ -445,44 +450,34 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
           for (int k = 0; k < 8; k++) { x[0][k] = red64(mb[k], R, pi); x[1][k] = red64(ma[k], R, pi); }
           ntt_inv32<N, 2>(x, sb, tid, it, pr, pr2, R.zero);
+          // CRT, accumulated prime by prime (thread-private coefficients tid + T k):
+          //   t_i = r_i (P/p_i)^{-1} mod p_i,  V = sum_i t_i P/p_i - round(sum_i t_i / p_i) P,
+          // exact because |V| < P/4 keeps sum t_i/p_i within 1/4 of an integer (fp32 is ample);
+          // acc += V mod Q  as  acc += t_i (P/p_i mod Q) per prime, then - k (P mod Q).
 #pragma unroll
           for (int c = 0; c < 2; c++) {
-            u32* s0 = st0 + c * N;
-            u32* s1 = st1 + c * N;
+            u64* sa = sacc + c * N;
+            float* sf = sfr + c * N;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
               const int pos = tid + T * k;
-              const u32 rv = csub32(x[c][k], pr);                      // residue mod p_pi, [0, p)
+              const u32 rv = csub32(x[c][k], pr);                                    // r_i in [0, p)
+              const u32 t = csub32(shoup32(rv, R.y[pi], R.ys[pi], pr), pr);          // t_i in [0, p)
+              const float ft = (__int_as_float(0x4B000000 | (t >> 5)) - 8388608.0f) * R.fs[pi];
+              const u64 add = csub(shoup64_32(t, R.M[pi], R.Ms[pi], Q), Q);        // t_i P/p_i mod Q
+              u64 a = add_mod(sa[pos], add, Q);
               if (pi == 0) {
-                s0[pos] = rv;
-              } else if (pi == 1) {
-                const u32 c0 = s0[pos];
-                const u32 c0m = csub32(c0, R.p[1]);                    // c0 mod p1 (p0 < 2 p1)
-                const u32 c1 = csub32(shoup32(rv + R.p[1] - c0m, R.g01, R.g01s, R.p[1]), R.p[1]);
-                if (NP == 2) {
-                  // V = c0 + c1 p0 - [c1 > p1/2] P  (mod Q)
-                  u64 v = shoup64_32(c0, R.m0, R.m0s, Q) + shoup64_32(c1, R.m1, R.m1s, Q);   // < 4Q
-                  if (c1 > (R.p[1] >> 1)) v += Q - R.pmq;                                    // V < 0
-                  v = csub(csub(v, Q << 2), Q << 1);
-                  v = csub(v, Q);
-                  sacc[c * N + pos] = add_mod(sacc[c * N + pos], v, Q);
-                } else {
-                  s1[pos] = c1;
-                }
+                sf[pos] = ft;
+              } else if (pi < NP - 1) {
+                sf[pos] += ft;
               } else {
-                const u32 c0 = s0[pos], c1 = s1[pos];
-                const u32 c0m = csub32(c0, R.p[2]);
-                const u32 c1m = csub32(c1, R.p[2]);
-                const u32 u1 = shoup32(rv + R.p[2] - c0m, R.g02, R.g02s, R.p[2]);   // [0, 2 p2)
-                const u32 u2 = shoup32(c1m, R.g12, R.g12s, R.p[2]);                 // [0, 2 p2)
-                const u32 c2 = csub32(csub32(u1 + R.p2[2] - u2, R.p2[2]), R.p[2]);  // [0, p2)
-                u64 v = shoup64_32(c0, R.m0, R.m0s, Q) + shoup64_32(c1, R.m1, R.m1s, Q) +
-                        shoup64_32(c2, R.m2, R.m2s, Q);                                     // < 6Q
-                if (c2 > (R.p[2] >> 1)) v += Q - R.pmq;                                     // V < 0
-                v = csub(csub(v, Q << 2), Q << 1);
-                v = csub(v, Q);
-                sacc[c * N + pos] = add_mod(sacc[c * N + pos], v, Q);
+                const u32 kk = (u32)__float2int_rn(sf[pos] + ft);                   // 0 .. NP
+                u64 kq = (u64)kk * R.pq;                                            // < (NP+1) Q
+                kq = csub(csub(kq, Q << 1), Q);
+                kq = csub(kq, Q);
+                a = sub_mod(a, kq, Q);
               }
+              sa[pos] = a;
             }
           }
         }
