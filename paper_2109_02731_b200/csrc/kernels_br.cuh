@@ -464,18 +464,20 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
               const u32 rv = csub32(x[c][k], pr);                                    // r_i in [0, p)
               const u32 t = csub32(shoup32(rv, R.y[pi], R.ys[pi], pr), pr);          // t_i in [0, p)
               const float ft = (__int_as_float(0x4B000000 | (t >> 5)) - 8388608.0f) * R.fs[pi];
-              const u64 add = csub(shoup64_32(t, R.M[pi], R.Ms[pi], Q), Q);        // t_i P/p_i mod Q
-              u64 a = add_mod(sa[pos], add, Q);
+              // acc stays unreduced until the last prime: < Q + 2Q per prime (< 7Q), then
+              // + (NP+1) Q - k (P mod Q) < 11Q < 2^58 and one reduction to [0, Q)
+              u64 a = sa[pos] + shoup64_32(t, R.M[pi], R.Ms[pi], Q);              // + t_i P/p_i (mod Q)
               if (pi == 0) {
                 sf[pos] = ft;
               } else if (pi < NP - 1) {
                 sf[pos] += ft;
               } else {
                 const u32 kk = (u32)__float2int_rn(sf[pos] + ft);                   // 0 .. NP
-                u64 kq = (u64)kk * R.pq;                                            // < (NP+1) Q
-                kq = csub(csub(kq, Q << 1), Q);
-                kq = csub(kq, Q);
-                a = sub_mod(a, kq, Q);
+                a += (u64)(NP + 1) * Q - (u64)kk * R.pq;                            // pq < Q
+                a = csub(a, Q << 3);
+                a = csub(a, Q << 2);
+                a = csub(a, Q << 1);
+                a = csub(a, Q);
               }
               sa[pos] = a;
             }
