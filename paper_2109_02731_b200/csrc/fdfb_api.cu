@@ -177,7 +177,7 @@ template <int N, int NP, bool GIN>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
                        const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
   constexpr int T = N / 8;
-  const size_t sm = 49 * (size_t)N;            // sacc 16N + sd 16N + exchange 2 planes 9N + CRT sums 8N bytes
+  const size_t sm = 50 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange buffers x 2 planes 9N bytes
   // function attributes are per device: set on every launch (host-side, ~µs), not once per process
   cudaFuncSetAttribute(k_blind_rotate<N, NP, GIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int per_sm = 0;
@@ -435,7 +435,7 @@ static int setup_rns(fdfb_ctx* c) {
     }
     R.y[i] = (u32)h_inv(Pi_p, primes[i]); R.ys[i] = s32(R.y[i], primes[i]);
     R.M[i] = Pi_q; R.Ms[i] = shoup_of(Pi_q, Q);
-    R.fs[i] = (float)(32.0 / (double)primes[i]);
+    R.f16[i] = (u32)((1ULL << 36) / primes[i]);
   }
   R.pq = (u64)(P % Q);
   ft.insert(ft.end(), it.begin(), it.end());

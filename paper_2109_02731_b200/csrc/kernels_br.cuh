@@ -56,7 +56,7 @@ struct RnsParams {
   u32 y[RNS_MAXP], ys[RNS_MAXP];          // y_i and its Shoup companion
   u64 M[RNS_MAXP], Ms[RNS_MAXP];          // (P/p_i) mod Q and its 64-bit Shoup companion
   u64 pq;                                 // P mod Q
-  float fs[RNS_MAXP];                     // 32 / p_i  (t_i / p_i from the top 23 bits of t_i)
+  u32 f16[RNS_MAXP];                      // floor(2^36 / p_i): 16 t_i / p_i = umulhi(t_i, f16) (+ < 1)
   u32 zero;                               // 0, opaque to the compiler (see bfw32)
   const uint4* ftab;                      // [np][GROUPS][8 pairs] forward (w, w') u32
   const uint4* itab;                      // inverse
@@ -341,8 +341,8 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
   extern __shared__ u64 smem[];
   u64* sacc = smem;                          // [b | a], natural order, canonical mod Q
   u64* sd = smem + 2 * N;                    // d = acc X^e - acc, both halves (thread-private slots)
-  u32* sb = (u32*)(smem + 4 * N);            // NTT exchange buffer: 2 planes of 9N/8 words
-  float* sfr = (float*)(sb + 2 * Lay<N>::WORDS);   // CRT: running sum of t_i / p_i per output [2][N]
+  u32* sbuf = (u32*)(smem + 4 * N);          // NTT exchange buffers: 2 x (2 planes of 9N/8 words),
+                                             // alternating per transform (no barrier between transforms)
   const int tid = threadIdx.x;
   const u64 Q = p.Q;
   const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
@@ -370,6 +370,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
         // exponent -abar_i u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
+        int xb = 0;                                // exchange buffer of the next transform
         __syncthreads();                           // acc of the previous step complete
         // d = acc X^e - acc for both halves, once per CMux (thread-private slots of sd; the
         // epilogues below may then update acc prime by prime)
@@ -426,8 +427,10 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 x[0][k] = (u32)(dv >> sh) & dmask;
                 x[1][k] = two ? (u32)(dv >> (sh + logL)) & dmask : 0u;
               }
-              if (pi > 0 || half > 0 || r > 0) __syncthreads();   // previous readers of sb done
-              ntt_fwd32<N, 2>(x, sb, tid, ft, pr, pr2, R.zero);
+              // transform k writes buffer k % 2 only after its own CTA barrier has seen every warp
+              // finish transform k - 1, whose buffer laggards may still read: no barrier here
+              ntt_fwd32<N, 2>(x, sbuf + xb * 2 * Lay<N>::WORDS, tid, ft, pr, pr2, R.zero);
+              xb ^= 1;
 #pragma unroll
               for (int v = 0; v < 2; v++) {
                 if (v == 1 && !two) break;
@@ -449,31 +452,29 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           u32 x[2][8];
 #pragma unroll
           for (int k = 0; k < 8; k++) { x[0][k] = red64(mb[k], R, pi); x[1][k] = red64(ma[k], R, pi); }
-          ntt_inv32<N, 2>(x, sb, tid, it, pr, pr2, R.zero);
+          ntt_inv32<N, 2>(x, sbuf + xb * 2 * Lay<N>::WORDS, tid, it, pr, pr2, R.zero);
+          xb ^= 1;
           // CRT, accumulated prime by prime (thread-private coefficients tid + T k):
           //   t_i = r_i (P/p_i)^{-1} mod p_i,  V = sum_i t_i P/p_i - round(sum_i t_i / p_i) P,
-          // exact because |V| < P/4 keeps sum t_i/p_i within 1/4 of an integer (fp32 is ample);
-          // acc += V mod Q  as  acc += t_i (P/p_i mod Q) per prime, then - k (P mod Q).
+          // exact because |V| < 3P/8 keeps sum t_i/p_i within 3/8 of an integer.  acc += V mod Q
+          // as acc += t_i (P/p_i mod Q) per prime (unreduced: < 7Q < 2^57), while the sum of
+          // floor(16 t_i / p_i) (<= 45, error < 3/16) rides in bits 58..63 of the same word.
 #pragma unroll
           for (int c = 0; c < 2; c++) {
             u64* sa = sacc + c * N;
-            float* sf = sfr + c * N;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
               const int pos = tid + T * k;
               const u32 rv = csub32(x[c][k], pr);                                    // r_i in [0, p)
               const u32 t = csub32(shoup32(rv, R.y[pi], R.ys[pi], pr), pr);          // t_i in [0, p)
-              const float ft = (__int_as_float(0x4B000000 | (t >> 5)) - 8388608.0f) * R.fs[pi];
-              // acc stays unreduced until the last prime: < Q + 2Q per prime (< 7Q), then
-              // + (NP+1) Q - k (P mod Q) < 11Q < 2^58 and one reduction to [0, Q)
+              const u32 f = __umulhi(t, R.f16[pi]);                                 // floor(16 t_i / p_i) - {0, 1}
               u64 a = sa[pos] + shoup64_32(t, R.M[pi], R.Ms[pi], Q);              // + t_i P/p_i (mod Q)
-              if (pi == 0) {
-                sf[pos] = ft;
-              } else if (pi < NP - 1) {
-                sf[pos] += ft;
+              if (pi < NP - 1) {
+                a += (u64)f << 58;
               } else {
-                const u32 kk = (u32)__float2int_rn(sf[pos] + ft);                   // 0 .. NP
-                a += (u64)(NP + 1) * Q - (u64)kk * R.pq;                            // pq < Q
+                const u32 kk = ((u32)(a >> 58) + f + 8) >> 4;                       // round(sum t_i / p_i)
+                a &= (1ull << 58) - 1;
+                a += (u64)(NP + 1) * Q - (u64)kk * R.pq;                            // kk <= NP, pq < Q
                 a = csub(a, Q << 3);
                 a = csub(a, Q << 2);
                 a = csub(a, Q << 1);
