@@ -9,15 +9,15 @@
 // Exact RNS evaluation of the external product.  The products D_r * K (negacyclic, over
 // the integers, K in [0, Q)) have |coefficients| < 2 ell N (L-1) Q (< 2^82 at the Large
 // configuration), so they are computed exactly modulo NP word-size NTT primes
-// (P = prod p_i > 2 * bound; p_i < 2^29) with 32-bit Harvey/Shoup arithmetic, and the signed integer
-// result is recovered by Garner CRT and reduced mod Q.  The result is the same residue
+// (P = prod p_i > 8/3 bound; 2^27 < p_i < 2^28) with 32-bit Harvey/Shoup arithmetic, and the signed
+// integer result is recovered by CRT and reduced mod Q.  The result is the same residue
 // vector as the schoolbook definition (bit-exact with any correct evaluation); it costs
 // ~4 IMAD slots per 30-bit butterfly instead of ~16-22 for a 54-bit Shoup butterfly.
 //
 // Per CMux and prime p: 2 ell forward NTT_p of the digit polynomials (registers, radix-8
 // passes, one smem exchange each, u32), lazy 64-bit MAC against the NTT_p-domain key
-// (u32, N^{-1} folded in), one reduction, 2 inverse NTT_p; after the last prime, Garner
-// CRT per coefficient and acc += V mod Q.
+// (u32, N^{-1} folded in), one reduction, 2 inverse NTT_p, and the prime's CRT term added
+// to acc (the rounding k = round(sum t_i / p_i) and acc -= k P mod Q after the last prime).
 //
 // Twiddles: pass-grouped tables of (w, w') u32 pairs per prime (fdfb_api.cu
 // make_rns_tables), 8 pairs per group (7 used) -> one base per pass, 16-byte loads.
