@@ -414,7 +414,6 @@ static int setup_rns(fdfb_ctx* c) {
     R.p[i] = (u32)pr; R.p2[i] = (u32)(2 * pr);
     R.r32[i] = (u32)((1ULL << 32) % pr); R.r32s[i] = (u32)(((u64)R.r32[i] << 32) / pr);
     R.b32[i] = (u32)((1ULL << 32) / pr);
-    R.ninv[i] = (u32)h_inv(N, pr); R.ninvs[i] = (u32)(((u64)R.ninv[i] << 32) / pr);
     const u64 psi = h_primroot_2n(pr, N);
     if (!psi) return FDFB_E_UNSUPPORTED;
     const u64 psii = h_inv(psi, pr);
@@ -434,6 +433,8 @@ static int setup_rns(fdfb_ctx* c) {
       Pi_p = h_mulmod(Pi_p, primes[j] % primes[i], primes[i]);
     }
     R.y[i] = (u32)h_inv(Pi_p, primes[i]); R.ys[i] = s32(R.y[i], primes[i]);
+    // the key carries N^{-1} y_i: the inverse NTT then yields t_i = r_i y_i directly
+    R.ninv[i] = (u32)h_mulmod(h_inv(N, primes[i]), R.y[i], primes[i]); R.ninvs[i] = s32(R.ninv[i], primes[i]);
     R.M[i] = Pi_q; R.Ms[i] = shoup_of(Pi_q, Q);
     R.f16[i] = (u32)((1ULL << 36) / primes[i]);
   }

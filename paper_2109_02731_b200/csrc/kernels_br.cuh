@@ -16,7 +16,7 @@
 //
 // Per CMux and prime p: 2 ell forward NTT_p of the digit polynomials (registers, radix-8
 // passes, one smem exchange each, u32), lazy 64-bit MAC against the NTT_p-domain key
-// (u32, N^{-1} folded in), one reduction, 2 inverse NTT_p, and the prime's CRT term added
+// (u32, N^{-1} (P/p)^{-1} folded in), one reduction, 2 inverse NTT_p, and the prime's CRT term added
 // to acc (the rounding k = round(sum t_i / p_i) and acc -= k P mod Q after the last prime).
 //
 // Twiddles: pass-grouped tables of (w, w') u32 pairs per prime (fdfb_api.cu
@@ -51,7 +51,7 @@ struct RnsParams {
   u32 p[RNS_MAXP], p2[RNS_MAXP];          // primes, 2p
   u32 r32[RNS_MAXP], r32s[RNS_MAXP];      // 2^32 mod p and its Shoup companion
   u32 b32[RNS_MAXP];                      // floor(2^32 / p)  (reduction of a 32-bit word)
-  u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} mod p (key import)
+  u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} y_i mod p (key import; y_i: CRT below)
   // CRT: t_i = r_i y_i mod p_i with y_i = (P/p_i)^{-1} mod p_i;  V = sum t_i M_i - k P
   u32 y[RNS_MAXP], ys[RNS_MAXP];          // y_i and its Shoup companion
   u64 M[RNS_MAXP], Ms[RNS_MAXP];          // (P/p_i) mod Q and its 64-bit Shoup companion
@@ -465,8 +465,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
             for (int k = 0; k < 8; k++) {
               const int pos = tid + T * k;
-              const u32 rv = csub32(x[c][k], pr);                                    // r_i in [0, p)
-              const u32 t = csub32(shoup32(rv, R.y[pi], R.ys[pi], pr), pr);          // t_i in [0, p)
+              const u32 t = csub32(x[c][k], pr);          // t_i = r_i y_i in [0, p) (y_i folded into brK)
               const u32 f = __umulhi(t, R.f16[pi]);                                 // floor(16 t_i / p_i) - {0, 1}
               u64 a = sa[pos] + shoup64_32(t, R.M[pi], R.Ms[pi], Q);              // + t_i P/p_i (mod Q)
               if (pi < NP - 1) {
@@ -493,7 +492,9 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 }
 
 // brK import: canonical RGSW rows (coefficient domain, [0, Q)) -> for each prime p_i:
-// NTT_p(row mod p_i) * N^{-1} mod p_i, in [0, p_i).  One CTA (T threads) per (poly, prime);
+// NTT_p(row mod p_i) * N^{-1} y_i mod p_i, in [0, p_i)  (y_i = (P/p_i)^{-1} mod p_i, the CRT
+// weight, so the inverse transform of the MAC yields t_i = r_i y_i directly).
+// One CTA (T threads) per (poly, prime);
 // poly = row*2 + col of the canonical [rows][2][N] block starting at flat row `row0`.
 template <int N>
 __global__ void __launch_bounds__(N / 8)
