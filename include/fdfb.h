@@ -54,7 +54,7 @@ enum {
 typedef struct fdfb_params {
   uint32_t N;          /* ring degree, power of two in [256, 2048]                         */
   uint32_t n;          /* LWE dimension, 1..4096                                           */
-  uint64_t Q;          /* RLWE prime, Q = 1 mod 2N, Q < 2^62              */
+  uint64_t Q;          /* RLWE prime, Q = 1 mod 2N, Q < 2^55  (the paper: 2^54) */
   uint32_t log_q_lwe;  /* LWE modulus q_lwe = 2^log_q_lwe, 8..62 (reading c.3)   */
   uint32_t lwe_key;    /* 0: binary s, u = [1];  1: ternary s, u = [-1, 1] */
   uint32_t rlwe_key;   /* 0: binary, 1: ternary ring secret                                */

@@ -322,9 +322,10 @@ static size_t canon_ksk_bytes(const fdfb_params& p) { return (size_t)p.N * p.ell
 // ------------------------------------------------------------------ context
 static int validate(const fdfb_params* p) {
   if (!p) return FDFB_E_NULL;
+  // Q < 2^55: the blind rotation's CRT accumulates up to 7Q below the rounding bits 58..63
   if (!(p->N == 256 || p->N == 512 || p->N == 1024 || p->N == 2048)) return FDFB_E_DIMENSION;
   if (p->n < 1 || p->n > 4096) return FDFB_E_DIMENSION;
-  if (p->Q < 3 || p->Q >= (1ULL << 56) || !h_is_prime(p->Q) || (p->Q - 1) % (2 * (u64)p->N)) return FDFB_E_NON_NTT_MODULUS;
+  if (p->Q < 3 || p->Q >= (1ULL << 55) || !h_is_prime(p->Q) || (p->Q - 1) % (2 * (u64)p->N)) return FDFB_E_NON_NTT_MODULUS;
   if (p->log_q_lwe < 8 || p->log_q_lwe > 62 || p->log_q_lwe < (uint32_t)ceil_log2(2 * p->N) + 1) return FDFB_E_DIMENSION;
   if (p->lwe_key > 1 || p->rlwe_key > 1) return FDFB_E_UNSUPPORTED;
   const int qb = bits_of(p->Q - 1) > 0 ? ceil_log2(p->Q) : 1;

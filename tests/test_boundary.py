@@ -77,6 +77,7 @@ def test_parameter_validation_before_device_use():
     assert rc(N=3000) == -3                                   # N not a power of two in range
     assert rc(Q=base["Q"] + 2) == -2                          # not prime
     assert rc(Q=2**31 - 1) == -2                              # prime, but not 1 mod 2N
+    assert rc(Q=72057594037641217) == -2                      # NTT prime, but >= 2^55 (BR CRT headroom)
     assert rc(ell_rgsw=3) == -4                               # ell != ceil(54 / 14)
     assert rc(ell_ks=12) == -4
     assert rc(t=3) == -6                                      # t does not divide 2N
