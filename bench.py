@@ -52,6 +52,8 @@ def parse():
                                                                  "shiftboot"])
     ap.add_argument("--luts", type=int, default=4, help="functions per input for --workload multilut")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
+    ap.add_argument("--box", action="store_true",
+                    help="Box-scale: 65536 ciphertexts in total, sharded over the ranks (strong scaling)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="end-to-end steps (default: --steps)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -646,6 +648,10 @@ def main():
             dist.init_process_group(args.dist_backend)
     cfg = synth.load_config(args.config)
     B = args.batch or cfg["batch"]
+    if args.box:                               # BASELINE Box-scale: 65536 over 1/2/4/8 GPUs
+        if 65536 % world:
+            raise SystemExit("--box needs a world size dividing 65536")
+        B = 65536 // world
     ctx = Context(cfg, local)
     stream = torch.cuda.current_stream()
     if args.workload == "multilut":
@@ -724,12 +730,14 @@ def main():
         roof.update({"kernel_ms_per_step": kms_step, "kernel_launches": k_launches,
                      "kernel_share_of_step": kms_step / ms_step})
         cfgd = W.config()
+        if args.box:
+            cfgd["workload"] = cfgd.get("workload", "") + "-box65536"
         cfgd.update({"per_gpu_batch": B, "global_batch": B * world, "parallelism": "dp%d" % world,
                      "l2": "flushed between timed steps (256 MB write)", "keys_resident_bytes": W.key_bytes})
         line = {
             "metric": W.metric, "value": value, "unit": W.unit,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "higher_is_better": True, "scaling": "strong" if args.box else "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic", "config": cfgd, "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": W.unit, "steps": e2e_steps,
                     "h2d_bytes_per_step": W.io_bytes, "d2h_bytes_per_step": getattr(W, "io_out_bytes", W.io_bytes),
