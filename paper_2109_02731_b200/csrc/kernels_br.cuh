@@ -74,7 +74,7 @@ FDFB_DEV u32 csub32(u32 x, u32 m) { return min(x, x - m); }
 // Conditional subtractions are unsigned min (VIADDMNMX).  Needs 6p < 2^32 (p < 2^29).
 // Forward butterflies are lazy (no reduction): a stage adds at most 2p to the bound.  With
 // p < 2^28 values may grow to 16p < 2^32, so the transform tracks its bound at compile time
-// and reduces (red16, [0, 16p) -> [0, 2p)) only before a pass that would overflow: once per
+// and subtracts 8p conditionally (red8p_all) only before a pass that would overflow: twice per
 // 2048-point transform instead of a conditional subtraction per butterfly.
 FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // CT, +2p per stage
   const u32 t = shoup32(Y, w, ws, p);                                   // [0, 2p)
@@ -122,14 +122,18 @@ FDFB_DEV void fwd8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
     for (int k = 0; k < 4; k++) bfw32(x[v][2 * k], x[v][2 * k + 1], t.w[3 + k], t.s[3 + k], p, p2, z);
   }
 }
-// bound bookkeeping (in units of p): a radix-8 pass adds 6, the final pass 2 PLAST
+// bound bookkeeping (in units of p): a radix-8 pass adds 6, the final pass 2 PLAST.  Before a
+// pass that would leave [0, 16p), one conditional subtraction of 8p maps [0, B p) to
+// [0, max(8, B - 8) p) (B <= 16): one VIADDMNMX per value instead of a full reduction.
 template <int V>
-FDFB_DEV void red16_all(u32 (&x)[V][8], u32 p2) {
+FDFB_DEV void red8p_all(u32 (&x)[V][8], u32 p2) {
+  const u32 p8 = p2 << 2;
 #pragma unroll
   for (int v = 0; v < V; v++)
 #pragma unroll
-    for (int k = 0; k < 8; k++) x[v][k] = red16(x[v][k], p2);
+    for (int k = 0; k < 8; k++) x[v][k] = csub32(x[v][k], p8);
 }
+constexpr int after_red8p(int b) { return b - 8 > 8 ? b - 8 : 8; }
 template <int V>
 FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   Tw8 t; load_tw8(t, g);
@@ -241,10 +245,10 @@ FDFB_DEV void fwd_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p,
   if constexpr (q < BrShape<N>::NMID) {
     constexpr int T1 = N >> (3 * q + 3);
     constexpr bool RED = BOUND + 6 > 16;              // this pass would leave [0, 16p): reduce first
-    constexpr int OUT = (RED ? 2 : BOUND) + 6;
+    constexpr int OUT = (RED ? after_red8p(BOUND) : BOUND) + 6;
     const int B = qbase<N, q>(tid);
     xload<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
-    if constexpr (RED) red16_all<V>(x, p2);
+    if constexpr (RED) red8p_all<V>(x, p2);
     fwd8_32<V>(x, tab + 4 * (BrShape<N>::grp(q) + tid / T1), p, p2, z);
     __syncwarp();
     xstore<N, q, V>(x, sb, lay_base<N, q>(B), T1);
@@ -256,7 +260,7 @@ FDFB_DEV void fwd_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p,
 template <int N, int q, int BOUND>
 constexpr int fwd_bound_before_last() {
   if constexpr (q < BrShape<N>::NMID) {
-    constexpr int OUT = ((BOUND + 6 > 16) ? 2 : BOUND) + 6;
+    constexpr int OUT = ((BOUND + 6 > 16) ? after_red8p(BOUND) : BOUND) + 6;
     return fwd_bound_before_last<N, q + 1, OUT>();
   } else {
     return BOUND;
@@ -289,14 +293,14 @@ FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 
   fwd_mid<N, 1, V, 8>(x, sb, tid, tab, p, p2, z);
   xload<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
   constexpr int BL = fwd_bound_before_last<N, 1, 8>();
-  if constexpr (BL + 2 * S::PLAST > 16) red16_all<V>(x, p2);
+  if constexpr (BL + 2 * S::PLAST > 16) red8p_all<V>(x, p2);
   fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
 }
 // bound (in p) of the forward transform's outputs
 template <int N>
 constexpr int fwd_out_bound() {
   constexpr int BL = fwd_bound_before_last<N, 1, 8>();
-  return ((BL + 2 * BrShape<N>::PLAST > 16) ? 2 : BL) + 2 * BrShape<N>::PLAST;
+  return ((BL + 2 * BrShape<N>::PLAST > 16) ? after_red8p(BL) : BL) + 2 * BrShape<N>::PLAST;
 }
 
 // Inverse NTT mod p (unscaled) of V polynomials. In: slot 8 tid + k, [0, 2p).  Out:
@@ -338,6 +342,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                int s_begin) {
   using S = BrShape<N>;
   constexpr int T = S::T;
+  static_assert(fwd_out_bound<N>() <= 16, "forward outputs must stay below 16p < 2^32 (MAC bound)");
   extern __shared__ u64 smem[];
   u64* sacc = smem;                          // [b | a], natural order, canonical mod Q
   u64* sd = smem + 2 * N;                    // d = acc X^e - acc, both halves (thread-private slots)
