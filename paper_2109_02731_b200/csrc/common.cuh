@@ -26,6 +26,7 @@ struct DevParams {
   const u64* itw;  const u64* itwp;   // inverse twiddles psi^{-bitrev(k)}
   u64 ninv, ninvp;                    // N^{-1} mod Q and its Shoup companion
   const u64* cdt;                     // 2*cdt_T CDT thresholds
+  u64 qbar, qbias;                    // floor(2^64 / Q); a multiple of Q >= 2^31 (horner_mod)
 };
 
 // ---------------------------------------------------------------- modular arithmetic
@@ -43,6 +44,16 @@ FDFB_DEV u64 neg_mod(u64 a, u64 Q) { return a ? Q - a : 0; }
 FDFB_DEV u64 mul_mod_slow(u64 a, u64 b, u64 Q) {
   unsigned __int128 p = (unsigned __int128)a * b;
   return (u64)(p % Q);
+}
+// One Horner step of an exact digit recombination mod Q (GEMM epilogues):
+// acc <- (acc 2^s + d) mod Q for acc in [0, Q), s <= 8, |d| < 2^31, Q < 2^55.
+// x = acc 2^s + d + qbias < 2^64 is reduced by Barrett with qbar = floor(2^64 / Q):
+// the estimate is at most 2 below floor(x / Q), so x - q Q lies in [0, 3Q).
+FDFB_DEV u64 horner_mod(u64 acc, int s, long long d, const DevParams& p) {
+  const u64 x = (acc << s) + (u64)(d + (long long)p.qbias);
+  const u64 q = __umul64hi(x, p.qbar);
+  const u64 r = x - q * p.Q;
+  return csub(csub(r, p.Q << 1), p.Q);
 }
 FDFB_DEV u64 from_signed(long long v, u64 Q) {
   long long r = v % (long long)Q;

@@ -309,7 +309,7 @@ static int ks_gemm(const fdfb_ctx* c, const void* key_dev, size_t canon_bytes, c
     int rc = lt_gemm_i8(c, GK, A, D, rows * g.NL, g.Kd, g.Nout, lt_ws, kclass, st);
     if (rc) return rc;
     const size_t tot = (size_t)rows * g.W;
-    k_ks_gemm_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(D, in, rows, N, g, c->prm.Q, qmask,
+    k_ks_gemm_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, D, in, rows, N, g, c->prm.Q, qmask,
                                                                      out + (size_t)o * g.W);
     CKL(c);
   }
@@ -505,6 +505,8 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   d.tw = c->d_tables; d.twp = c->d_tables + N; d.itw = c->d_tables + 2 * N; d.itwp = c->d_tables + 3 * N;
   d.cdt = c->d_tables + 4 * N;
   d.ninv = h_powmod(N, Q - 2, Q); d.ninvp = shoup_of(d.ninv, Q);
+  d.qbar = (u64)((((u128)1) << 64) / Q);
+  d.qbias = ((1ULL << 31) / Q + 1) * Q;
   // Montgomery: -Q^{-1} mod 2^64 (Newton), R^2 mod Q
   u64 inv = 1;
   for (int i = 0; i < 7; i++) inv *= 2 - Q * inv;

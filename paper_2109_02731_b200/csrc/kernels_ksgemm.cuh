@@ -58,11 +58,25 @@ __global__ void k_ks_gemm_bits(const u64* __restrict__ lwe, int rows, int N, int
   }
 }
 // out[g][w] = [b_g]_{w=0} - value(D rows of g) mod q   (q = Q prime if qmask == 0, else 2^w via qmask)
-__global__ void k_ks_gemm_finish(const int* __restrict__ D, const u64* __restrict__ lwe, int rows, int N, KsGemm g,
+__global__ void k_ks_gemm_finish(DevParams dp, const int* __restrict__ D, const u64* __restrict__ lwe, int rows, int N, KsGemm g,
                                  u64 Q, u64 qmask, u64* __restrict__ out) {
   const size_t total = (size_t)rows * g.W;
   for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
     const int gi = (int)(x / g.W), w = (int)(x % g.W);
+    const u64 b = w == 0 ? __ldg(lwe + (size_t)gi * (N + 1)) : 0;
+    if (!qmask) {                                    // mod Q: Horner over 7-bit groups of 8-bit limbs
+      u64 vm = 0;
+#pragma unroll 1
+      for (int t = g.NL - 1; t >= 0; t--) {
+        const int* dr = D + ((size_t)gi * g.NL + t) * g.Nout + w;
+        u64 s = 0;
+#pragma unroll
+        for (int l = 6; l >= 0; l--) s = horner_mod(s, 8, dr[(size_t)l * g.Wpad], dp);
+        vm = add_mod(horner_mod(vm, 7, 0, dp), s, Q);
+      }
+      out[x] = b >= vm ? b - vm : b + Q - vm;
+      continue;
+    }
     __int128 v = 0;
 #pragma unroll 1
     for (int t = g.NL - 1; t >= 0; t--) {
@@ -72,15 +86,6 @@ __global__ void k_ks_gemm_finish(const int* __restrict__ D, const u64* __restric
       for (int l = 6; l >= 0; l--) s = s * 256 + dr[(size_t)l * g.Wpad];
       v = v * 128 + s;
     }
-    const u64 b = w == 0 ? __ldg(lwe + (size_t)gi * (N + 1)) : 0;
-    u64 r;
-    if (qmask) {
-      r = (b - (u64)v) & qmask;                      // two's complement wrap: exact mod 2^w
-    } else {
-      long long m = (long long)(v % (__int128)Q);     // in (-Q, Q)
-      const u64 vm = (u64)(m < 0 ? m + (long long)Q : m);
-      r = b >= vm ? b - vm : b + Q - vm;
-    }
-    out[x] = r;
+    out[x] = (b - (u64)v) & qmask;                   // two's complement wrap: exact mod 2^w
   }
 }

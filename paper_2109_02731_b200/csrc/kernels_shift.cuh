@@ -466,16 +466,14 @@ k_shift_gemm_finish(DevParams p, const u64* __restrict__ pk, PackLayout lay, con
 #pragma unroll
   for (int r = 0; r < CPT; r++) {
     const int x = tid + r * TPB;
-    __int128 vg = 0, vb = 0;
+    u64 vg = 0, vb = 0;                        // sum_l digit_l 256^l mod Q (Horner, Barrett)
 #pragma unroll
     for (int l = 6; l >= 0; l--) {
-      vg = vg * 256 + dg[(size_t)l * 2 * N + x];
-      vb = vb * 256 + db[(size_t)l * 2 * N + x];
+      vg = horner_mod(vg, 8, dg[(size_t)l * 2 * N + x], p);
+      vb = horner_mod(vb, 8, db[(size_t)l * 2 * N + x], p);
     }
-    long long rg = (long long)(vg % (__int128)Q), rb = (long long)(vb % (__int128)Q);
-    G[r] = (u64)(rg < 0 ? rg + (long long)Q : rg);
-    const u64 bs = (u64)(rb < 0 ? rb + (long long)Q : rb);
-    W[x] = add_mod(__ldg(U + x), bs, Q);
+    G[r] = vg;
+    W[x] = add_mod(__ldg(U + x), vb, Q);
   }
   __syncthreads();
   const u64* cth = ct + (size_t)c * 2 * N + (size_t)h * N;
@@ -553,21 +551,25 @@ __global__ void k_perm_bits(DevParams p, const u64* __restrict__ ct, const u32* 
     row[x] = v;
   }
 }
-// out[c] = ct[c] + sum_{i moved} X^{i-1} ([b_j - b_i, 0] - W_i), one CTA per (ciphertext, column)
+// out[c] = ct[c] + sum_{i moved} X^{i-1} ([b_j - b_i, 0] - W_i).  One CTA per (ciphertext,
+// column, slice of PERM_SLICES consecutive slots i): partial sums into part[c][h][slice][N]
+// (slice 0 also carries ct), summed by k_permute_reduce.
+#define PERM_SLICES 32
 template <int CPT>
 __global__ void __launch_bounds__(256)
-k_permute_finish(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, PermGemm g,
-                 const int* __restrict__ D, u64* __restrict__ out) {
+k_permute_partial(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, PermGemm g,
+                  const int* __restrict__ D, u64* __restrict__ part) {
   constexpr int TPB = 256;
-  const int N = p.N, cl = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int N = p.N, cl = blockIdx.x, h = blockIdx.y, sl = blockIdx.z, tid = threadIdx.x;
   const int c = c0 + cl;
   const u64 Q = p.Q;
   __shared__ u64 W[2048];
   const u64* cth = ct + (size_t)c * 2 * N;
   u64 acc[CPT];
 #pragma unroll
-  for (int r = 0; r < CPT; r++) acc[r] = cth[(size_t)h * N + tid + r * TPB];
-  for (int i = 1; i <= N; i++) {
+  for (int r = 0; r < CPT; r++) acc[r] = sl == 0 ? cth[(size_t)h * N + tid + r * TPB] : 0;
+  const int per = N / PERM_SLICES;
+  for (int i = 1 + sl * per; i <= (sl + 1) * per; i++) {
     int j = (int)perm[(size_t)c * N + (i - 1)];
     if (j < 1 || j > N || j == i) continue;                      // uniform across the CTA
     const int* drow = D + ((size_t)cl * N + (i - 1)) * g.Nout + (size_t)h * N;
@@ -575,11 +577,10 @@ k_permute_finish(DevParams p, const u64* __restrict__ ct, const u32* __restrict_
 #pragma unroll
     for (int r = 0; r < CPT; r++) {
       const int x = tid + r * TPB;
-      __int128 v = 0;
+      u64 v = 0;                                                  // sum_l digit_l 256^l mod Q
 #pragma unroll
-      for (int l = 6; l >= 0; l--) v = v * 256 + drow[(size_t)l * 2 * N + x];
-      long long m = (long long)(v % (__int128)Q);
-      u64 t = neg_mod((u64)(m < 0 ? m + (long long)Q : m), Q);     // -W_i
+      for (int l = 6; l >= 0; l--) v = horner_mod(v, 8, drow[(size_t)l * 2 * N + x], p);
+      u64 t = neg_mod(v, Q);                                      // -W_i
       if (h == 0 && x == 0) t = add_mod(t, sub_mod(cth[j - 1], cth[i - 1], Q), Q);   // + [b_j - b_i, 0]
       W[x] = t;
     }
@@ -587,8 +588,21 @@ k_permute_finish(DevParams p, const u64* __restrict__ ct, const u32* __restrict_
 #pragma unroll
     for (int r = 0; r < CPT; r++) acc[r] = add_mod(acc[r], rot_coeff(W, tid + r * TPB, i - 1, N, Q), Q);
   }
+  u64* o = part + (((size_t)cl * 2 + h) * PERM_SLICES + sl) * N;
 #pragma unroll
-  for (int r = 0; r < CPT; r++) out[(size_t)c * 2 * N + (size_t)h * N + tid + r * TPB] = acc[r];
+  for (int r = 0; r < CPT; r++) o[tid + r * TPB] = acc[r];
+}
+__global__ void k_permute_reduce(DevParams p, const u64* __restrict__ part, int c0, int nct, u64* __restrict__ out) {
+  const int N = p.N;
+  const size_t total = (size_t)nct * 2 * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    const size_t ch = x / N, w = x % N;                           // (local ciphertext, column), coefficient
+    const u64* src = part + ch * PERM_SLICES * N + w;
+    u64 s = 0;
+#pragma unroll 8
+    for (int k = 0; k < PERM_SLICES; k++) s = add_mod(s, __ldg(src + (size_t)k * N), p.Q);
+    out[(size_t)c0 * 2 * N + x] = s;
+  }
 }
 // Definition path for any L (small N): per (ciphertext, column) CTA, every moved slot's
 // v[j] - v[i] gathered from the canonical table, rotated by X^{i-1} and added.
