@@ -120,7 +120,7 @@ __global__ void k_pack_fixup(DevParams p, u64* __restrict__ pk, int ell, int L, 
 // ---------------------------------------------------------------------------
 // SampleExt mask coefficient a'_K[i] (1-based K, i, NSgn(x) = +1 iff x > 0)
 FDFB_DEV u64 sx_mask(const u64* a, int K, int i, int N, u64 Q) {
-  const int idx = ((K - i) % N + N) % N;
+  const int idx = (K - i) & (N - 1);                  // (K - i) mod N, N a power of two
   const u64 v = a[idx];
   return (K - i + 1 > 0) ? v : neg_mod(v, Q);
 }
@@ -408,35 +408,40 @@ __global__ void k_shift_gemm_key(DevParams p, const u64* __restrict__ pk, PackLa
     GK[((size_t)l * 2 * p.N + w) * g.Kpad + kk] = (int8_t)t;
   }
 }
-// Per-batch 0/1 matrix: rows 2c (G) and 2c+1 (Bs) of ciphertext c.
+// Per-batch 0/1 matrix: rows 2c (G) and 2c+1 (Bs) of ciphertext c.  Grid (ceil(N / blockDim), B):
+// thread t computes the SampleExt coefficients it needs once and writes their ell bits with
+// stride N-1 / N (coalesced across the warp for every bit j), no per-element division.
 __global__ void k_shift_bits(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ dd, int B, ShiftGemm g,
                              int8_t* __restrict__ A, int* __restrict__ status) {
   const int c = blockIdx.y;
   const int N = p.N, ell = p.ell_pack;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;       // 0 .. N-1
+  if (t >= N) return;
   int d = (int)dd[c];
   const bool ok = d >= 1 && d <= N - 1;
-  if (!ok) { if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, 1); d = 1; }
+  if (!ok) { if (t == 0) atomicOr(status, 1); d = 1; }
   const bool br1 = 2 * d <= N;
   const int m = br1 ? d : N - d, K1 = br1 ? N - d + 1 : 1, Km = K1 + m - 1;
   const u64* a = ct + (size_t)c * 2 * N + N;
   int8_t* rg = A + (size_t)(2 * c) * g.Kpad;
   int8_t* rb = rg + g.Kpad;
   const int s1 = ell * (N - 1);
-  for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < g.Kpad; kk += gridDim.x * blockDim.x) {
-    int8_t vg = 0, vb = 0;
-    if (ok && kk < s1) {
-      const int j = kk / (N - 1), t = kk % (N - 1);            // i' = t + 1
-      vg = (int8_t)((sx_mask(a, K1, t + 2, N, p.Q) >> j) & 1);
-      vb = (int8_t)((sx_mask(a, Km, t + 1, N, p.Q) >> j) & 1);
-    } else if (ok && kk < s1 + N) {
-      vg = (kk - s1) < m ? 1 : 0;
-    } else if (ok && kk < g.K) {
-      const int r = kk - s1 - N, j = r / N, k = r % N;
-      vg = k < m ? (int8_t)((a[K1 + k - 1] >> j) & 1) : 0;
+  if (t < N - 1) {                                            // Delta rows (i' = t + 1, bit j)
+    const u64 vgw = ok ? sx_mask(a, K1, t + 2, N, p.Q) : 0;
+    const u64 vbw = ok ? sx_mask(a, Km, t + 1, N, p.Q) : 0;
+    for (int j = 0; j < ell; j++) {
+      rg[j * (N - 1) + t] = (int8_t)((vgw >> j) & 1);
+      rb[j * (N - 1) + t] = (int8_t)((vbw >> j) & 1);
     }
-    rg[kk] = vg;
-    rb[kk] = vb;
   }
+  rg[s1 + t] = (int8_t)(ok && t < m);                         // E_m S0 rows
+  rb[s1 + t] = 0;
+  const u64 bw = (ok && t < m) ? a[K1 + t - 1] : 0;          // Toeplitz rows (bit j, k = t)
+  for (int j = 0; j < ell; j++) {
+    rg[s1 + N + j * N + t] = (int8_t)((bw >> j) & 1);
+    rb[s1 + N + j * N + t] = 0;
+  }
+  for (int kk = g.K + t; kk < g.Kpad; kk += N) { rg[kk] = 0; rb[kk] = 0; }
 }
 // Recombine digits (int32 D[row][l * 2N + w]) mod Q and assemble Shift's output, one CTA
 // of 256 threads per (ciphertext, column):  S = G + U - X^m (U + Bs);  P = [bsum, 0] - S;
@@ -531,24 +536,27 @@ __global__ void k_perm_gemm_key(DevParams p, const u64* __restrict__ pk, PackLay
   }
 }
 // rows r = c_local * N + (i-1) of a chunk of ciphertexts: A[r][k*ell + l] = bit_l(a'_j[k]) - bit_l(a'_i[k]),
-// j = pi(i); zero rows for fixed points (and flag an invalid permutation entry).
-__global__ void k_perm_bits(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, int nct,
-                            PermGemm g, int8_t* __restrict__ A, int* __restrict__ status) {
+// j = pi(i); zero rows for fixed points (and flag an invalid permutation entry).  One CTA of
+// (64, 4) threads per row: threadIdx.x = bit l, threadIdx.y strides over k (coalesced per k).
+__global__ void __launch_bounds__(256)
+k_perm_bits(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, int nct,
+            PermGemm g, int8_t* __restrict__ A, int* __restrict__ status) {
   const int N = p.N, ell = p.ell_pack;
-  const int r = blockIdx.y;                         // local row
+  const int r = blockIdx.x;                         // local row
   const int c = c0 + r / N, i = r % N + 1;          // 1-based slot
   int j = (int)perm[(size_t)c * N + (i - 1)];
-  if (j < 1 || j > N) { if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, 1); j = i; }
+  if (j < 1 || j > N) { if (threadIdx.x == 0 && threadIdx.y == 0) atomicOr(status, 1); j = i; }
   const u64* a = ct + (size_t)c * 2 * N + N;
   int8_t* row = A + (size_t)r * g.K;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.K; x += gridDim.x * blockDim.x) {
+  const int l = threadIdx.x;
+  if (l >= ell) return;
+  for (int k = 1 + threadIdx.y; k <= N; k += blockDim.y) {   // SampleExt index k (1-based)
     int8_t v = 0;
     if (j != i) {
-      const int k = x / ell + 1, l = x % ell;       // SampleExt index k (1-based), bit l
       const int bj = (int)((sx_mask(a, j, k, N, p.Q) >> l) & 1), bi = (int)((sx_mask(a, i, k, N, p.Q) >> l) & 1);
       v = (int8_t)(bj - bi);
     }
-    row[x] = v;
+    row[(k - 1) * ell + l] = v;
   }
 }
 // out[c] = ct[c] + sum_{i moved} X^{i-1} ([b_j - b_i, 0] - W_i).  One CTA per (ciphertext,
