@@ -519,11 +519,20 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
 
 extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   if (!c) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(c->device);                    // the context's allocations live on its device
+  {
+    std::lock_guard<std::mutex> g(c->tmu);     // timing events never read back
+    for (auto& e : c->tev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    c->tev.clear();
+  }
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
   cudaFree(c->d_rtab);
   if (c->lt) cublasLtDestroy(c->lt);
   delete c;
+  cudaSetDevice(cur);
 }
 
 static size_t brk_words(const fdfb_params& p) { return (size_t)p.n * (p.lwe_key ? 2 : 1) * 2 * p.ell_rgsw * 2 * p.N; }
@@ -542,6 +551,9 @@ extern "C" int fdfb_sizes(const fdfb_ctx* c, fdfb_sizes_t* o) {
   o->pack = shift_pack_bytes(p);
   return FDFB_OK;
 }
+
+// largest batch per call (keeps every derived count, e.g. B * ell_boot accumulators, in int)
+static const uint32_t kMaxBatch = 1u << 24;
 
 // workspace layout of fdfb_bootstrap_batch
 struct BootWs {
@@ -920,6 +932,7 @@ extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const vo
                                     void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (B > kMaxBatch) return FDFB_E_DIMENSION;
   if (!brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
   return bootstrap_impl(c, brk, bpk, ksk, rotp, 1, ct_in, ct_out, B, workspace, S(stream));
 }
@@ -929,6 +942,7 @@ extern "C" int fdfb_bootstrap_multi_batch(const fdfb_ctx* c, const void* brk, co
                                           uint32_t B, void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (B > kMaxBatch) return FDFB_E_DIMENSION;
   if (!brk || !bpk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
   if (k == 0) return FDFB_E_DIMENSION;
   return bootstrap_impl(c, brk, bpk, ksk, rotp, k, ct_in, ct_out, B, workspace, S(stream));
@@ -951,6 +965,7 @@ extern "C" int fdfb_bootstrap_tfhe_batch(const fdfb_ctx* c, const void* brk, con
                                          void* stream) {
   if (!c) return FDFB_E_NULL;
   if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (B > kMaxBatch) return FDFB_E_DIMENSION;
   if (!brk || !ksk || !rotp || !ct_in || !ct_out || !workspace) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   const fdfb_params& p = c->prm;
@@ -975,6 +990,7 @@ extern "C" int fdfb_bootstrap_batch_host(const fdfb_ctx* c, const void* brk, con
                                          void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (B == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (B > kMaxBatch) return FDFB_E_DIMENSION;
   if (!in_h || !out_h || !workspace) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   size_t bytes = (size_t)B * (c->prm.n + 1) * 8;
