@@ -129,6 +129,8 @@ def _ptr(t):
     if isinstance(t, torch.Tensor):
         if not t.is_contiguous():
             raise FdfbError("tensor must be contiguous")
+        if not t.is_cuda and t.numel() and not t.is_pinned():
+            raise FdfbError("host tensors must be pinned (device entry points take CUDA tensors)")
         return C.c_void_p(t.data_ptr())
     return t
 
