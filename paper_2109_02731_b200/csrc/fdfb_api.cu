@@ -415,6 +415,11 @@ static int setup_rns(fdfb_ctx* c) {
     R.p[i] = (u32)pr; R.p2[i] = (u32)(2 * pr);
     R.r32[i] = (u32)((1ULL << 32) % pr); R.r32s[i] = (u32)(((u64)R.r32[i] << 32) / pr);
     R.b32[i] = (u32)((1ULL << 32) / pr);
+    {                                              // -p^{-1} mod 2^32 by Newton iteration
+      u32 inv = (u32)pr;                           // p odd: p p = 1 mod 8
+      for (int it2 = 0; it2 < 5; it2++) inv *= 2u - (u32)pr * inv;
+      R.pinv[i] = 0u - inv;
+    }
     const u64 psi = h_primroot_2n(pr, N);
     if (!psi) return FDFB_E_UNSUPPORTED;
     const u64 psii = h_inv(psi, pr);
@@ -435,7 +440,8 @@ static int setup_rns(fdfb_ctx* c) {
     }
     R.y[i] = (u32)h_inv(Pi_p, primes[i]); R.ys[i] = s32(R.y[i], primes[i]);
     // the key carries N^{-1} y_i: the inverse NTT then yields t_i = r_i y_i directly
-    R.ninv[i] = (u32)h_mulmod(h_inv(N, primes[i]), R.y[i], primes[i]); R.ninvs[i] = s32(R.ninv[i], primes[i]);
+    R.ninv[i] = (u32)h_mulmod(h_mulmod(h_inv(N, primes[i]), R.y[i], primes[i]), (1ULL << 32) % primes[i], primes[i]);
+    R.ninvs[i] = s32(R.ninv[i], primes[i]);
     R.M[i] = Pi_q; R.Ms[i] = shoup_of(Pi_q, Q);
     R.f16[i] = (u32)((1ULL << 36) / primes[i]);
   }

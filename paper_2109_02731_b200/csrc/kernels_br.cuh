@@ -51,7 +51,8 @@ struct RnsParams {
   u32 p[RNS_MAXP], p2[RNS_MAXP];          // primes, 2p
   u32 r32[RNS_MAXP], r32s[RNS_MAXP];      // 2^32 mod p and its Shoup companion
   u32 b32[RNS_MAXP];                      // floor(2^32 / p)  (reduction of a 32-bit word)
-  u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} y_i mod p (key import; y_i: CRT below)
+  u32 pinv[RNS_MAXP];                     // -p^{-1} mod 2^32 (Montgomery reduction of the MAC)
+  u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} y_i 2^32 mod p (key import; y_i: CRT below)
   // CRT: t_i = r_i y_i mod p_i with y_i = (P/p_i)^{-1} mod p_i;  V = sum t_i M_i - k P
   u32 y[RNS_MAXP], ys[RNS_MAXP];          // y_i and its Shoup companion
   u64 M[RNS_MAXP], Ms[RNS_MAXP];          // (P/p_i) mod Q and its 64-bit Shoup companion
@@ -318,6 +319,15 @@ FDFB_DEV void ntt_inv32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 
   inv8_32<V>(x, tab, p, p2, z);
 }
 
+// Montgomery reduction of the MAC sum: s < 2^63 -> s 2^{-32} mod p in [0, 2p)  (the 2^32 is
+// folded into the RNS brK).  m = s_lo (-p^{-1}) mod 2^32 makes s + m p divisible by 2^32;
+// (s + m p) / 2^32 < 2^31 + p < 9p, brought to [0, 2p) by three conditional subtractions.
+FDFB_DEV u32 redc64(u64 s, const RnsParams& R, int i) {
+  const u32 m = (u32)s * R.pinv[i];
+  const u32 t = (u32)((s + (u64)m * R.p[i]) >> 32);
+  const u32 p2 = R.p2[i];
+  return csub32(csub32(csub32(t, p2 << 2), p2 << 1), p2);
+}
 // s < 2^63 -> s mod p in [0, 2p):  s1 2^32 + s0 = s1 (2^32 mod p) + s0
 FDFB_DEV u32 red64(u64 s, const RnsParams& R, int i) {
   const u32 s1 = (u32)(s >> 32), s0 = (u32)s;
@@ -456,7 +466,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           // both output columns through one paired inverse transform (warp-local start)
           u32 x[2][8];
 #pragma unroll
-          for (int k = 0; k < 8; k++) { x[0][k] = red64(mb[k], R, pi); x[1][k] = red64(ma[k], R, pi); }
+          for (int k = 0; k < 8; k++) { x[0][k] = redc64(mb[k], R, pi); x[1][k] = redc64(ma[k], R, pi); }
           ntt_inv32<N, 2>(x, sbuf + xb * 2 * Lay<N>::WORDS, tid, it, pr, pr2, R.zero);
           xb ^= 1;
           // CRT, accumulated prime by prime (thread-private coefficients tid + T k):
@@ -497,8 +507,9 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 }
 
 // brK import: canonical RGSW rows (coefficient domain, [0, Q)) -> for each prime p_i:
-// NTT_p(row mod p_i) * N^{-1} y_i mod p_i, in [0, p_i)  (y_i = (P/p_i)^{-1} mod p_i, the CRT
-// weight, so the inverse transform of the MAC yields t_i = r_i y_i directly).
+// NTT_p(row mod p_i) * N^{-1} y_i 2^32 mod p_i, in [0, p_i)  (y_i = (P/p_i)^{-1} mod p_i, the
+// CRT weight, so the inverse transform of the MAC yields t_i = r_i y_i directly; 2^32 cancels
+// the Montgomery reduction redc64).
 // One CTA (T threads) per (poly, prime);
 // poly = row*2 + col of the canonical [rows][2][N] block starting at flat row `row0`.
 template <int N>
