@@ -413,8 +413,6 @@ static int setup_rns(fdfb_ctx* c) {
   for (int i = 0; i < R.np; i++) {
     const u64 pr = primes[i];
     R.p[i] = (u32)pr; R.p2[i] = (u32)(2 * pr);
-    R.r32[i] = (u32)((1ULL << 32) % pr); R.r32s[i] = (u32)(((u64)R.r32[i] << 32) / pr);
-    R.b32[i] = (u32)((1ULL << 32) / pr);
     {                                              // -p^{-1} mod 2^32 by Newton iteration
       u32 inv = (u32)pr;                           // p odd: p p = 1 mod 8
       for (int it2 = 0; it2 < 5; it2++) inv *= 2u - (u32)pr * inv;
@@ -442,7 +440,7 @@ static int setup_rns(fdfb_ctx* c) {
     // the key carries N^{-1} y_i: the inverse NTT then yields t_i = r_i y_i directly
     R.ninv[i] = (u32)h_mulmod(h_mulmod(h_inv(N, primes[i]), R.y[i], primes[i]), (1ULL << 32) % primes[i], primes[i]);
     R.ninvs[i] = s32(R.ninv[i], primes[i]);
-    R.M[i] = Pi_q; R.Ms[i] = shoup_of(Pi_q, Q);
+    R.M[i] = Pi_q; R.Ms32[i] = (u32)(((u128)Pi_q << 32) / Q);
     R.f16[i] = (u32)((1ULL << 36) / primes[i]);
   }
   R.pq = (u64)(P % Q);

@@ -49,13 +49,12 @@ struct BrShape {
 struct RnsParams {
   int np;
   u32 p[RNS_MAXP], p2[RNS_MAXP];          // primes, 2p
-  u32 r32[RNS_MAXP], r32s[RNS_MAXP];      // 2^32 mod p and its Shoup companion
-  u32 b32[RNS_MAXP];                      // floor(2^32 / p)  (reduction of a 32-bit word)
   u32 pinv[RNS_MAXP];                     // -p^{-1} mod 2^32 (Montgomery reduction of the MAC)
   u32 ninv[RNS_MAXP], ninvs[RNS_MAXP];    // N^{-1} y_i 2^32 mod p (key import; y_i: CRT below)
   // CRT: t_i = r_i y_i mod p_i with y_i = (P/p_i)^{-1} mod p_i;  V = sum t_i M_i - k P
   u32 y[RNS_MAXP], ys[RNS_MAXP];          // y_i and its Shoup companion
-  u64 M[RNS_MAXP], Ms[RNS_MAXP];          // (P/p_i) mod Q and its 64-bit Shoup companion
+  u64 M[RNS_MAXP];                        // (P/p_i) mod Q
+  u32 Ms32[RNS_MAXP];                     // floor(M_i 2^32 / Q): Shoup quotient for 28-bit t_i
   u64 pq;                                 // P mod Q
   u32 f16[RNS_MAXP];                      // floor(2^36 / p_i): 16 t_i / p_i = umulhi(t_i, f16) (+ < 1)
   u32 zero;                               // 0, opaque to the compiler (see bfw32)
@@ -328,17 +327,11 @@ FDFB_DEV u32 redc64(u64 s, const RnsParams& R, int i) {
   const u32 p2 = R.p2[i];
   return csub32(csub32(csub32(t, p2 << 2), p2 << 1), p2);
 }
-// s < 2^63 -> s mod p in [0, 2p):  s1 2^32 + s0 = s1 (2^32 mod p) + s0
-FDFB_DEV u32 red64(u64 s, const RnsParams& R, int i) {
-  const u32 s1 = (u32)(s >> 32), s0 = (u32)s;
-  const u32 a = shoup32(s1, R.r32[i], R.r32s[i], R.p[i]);            // [0, 2p)
-  const u32 b = s0 - __umulhi(s0, R.b32[i]) * R.p[i];                // [0, 2p)
-  return csub32(a + b, R.p2[i]);                                     // [0, 2p)
-}
-// 64-bit Shoup with a 32-bit multiplicand: c * m mod Q in [0, 2Q)
-FDFB_DEV u64 shoup64_32(u32 c, u64 m, u64 ms, u64 Q) {
-  const u64 q = __umul64hi((u64)c, ms);
-  return (u64)c * m - q * Q;
+// c * m mod Q in [0, 2Q) for c < 2^28 with a 32-bit quotient companion ms32 = floor(m 2^32 / Q):
+// q = floor(c ms32 / 2^32) is floor(c m / Q) or one less (the truncation costs < c / 2^32 < 1/16)
+FDFB_DEV u64 shoup64_28(u32 c, u64 m, u32 ms32, u64 Q) {
+  const u32 q = __umulhi(c, ms32);
+  return (u64)c * m - (u64)q * Q;
 }
 
 // GIN = false: every step of the loop "for i in [n], j in [u]": CMux(brK[i,j], acc X^{-abar_i u_j}, acc).
@@ -458,7 +451,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
                   mb[k] += (u64)x[v][k] * kb[k];      // x < 16p < 2^32, K < p < 2^28: < 2^60 each,
-                  ma[k] += (u64)x[v][k] * ka[k];      // 2 ell <= 8 terms < 2^63 (red64's range)
+                  ma[k] += (u64)x[v][k] * ka[k];      // 2 ell <= 8 terms < 2^63 (redc64's range)
                 }
               }
             }
@@ -482,7 +475,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
               const int pos = tid + T * k;
               const u32 t = csub32(x[c][k], pr);          // t_i = r_i y_i in [0, p) (y_i folded into brK)
               const u32 f = __umulhi(t, R.f16[pi]);                                 // floor(16 t_i / p_i) - {0, 1}
-              u64 a = sa[pos] + shoup64_32(t, R.M[pi], R.Ms[pi], Q);              // + t_i P/p_i (mod Q)
+              u64 a = sa[pos] + shoup64_28(t, R.M[pi], R.Ms32[pi], Q);            // + t_i P/p_i (mod Q)
               if (pi < NP - 1) {
                 a += (u64)f << 58;
               } else {
