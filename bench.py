@@ -37,7 +37,7 @@ IMAD_PER_MODMUL = 16
 # DRAM traffic of k_blind_rotate<2048,3> per wave of 296 resident accumulators (2 per SM), from
 # `ncu --set full` (dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/ncu_full_blind_rotate.txt):
 # the RNS brK (0.81 GB) streams about twice per wave; the kernel is integer-pipe bound.
-BR_DRAM_BYTES_PER_WAVE = 1.5715e9 + 0.0125e9
+BR_DRAM_BYTES_PER_WAVE = 1.5734e9 + 0.0121e9
 
 
 def parse():

@@ -82,7 +82,6 @@ FDFB_DEV void bfw32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // 
   X = x + t + z;
   Y = x - t + p2;
 }
-FDFB_DEV u32 red8(u32 x, u32 p2, u32 p4) { return csub32(csub32(x, p4), p2); }   // [0, 8p) -> [0, 2p)
 FDFB_DEV u32 red16(u32 x, u32 p2) {                                                   // [0, 16p) -> [0, 2p)
   return csub32(csub32(csub32(x, p2 << 2), p2 << 1), p2);
 }
