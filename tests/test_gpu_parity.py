@@ -159,6 +159,25 @@ def test_blind_rotate_matches_oracle(name, count):
         assert np.array_equal(got2[0], ref)
 
 
+@pytest.mark.parametrize("logL,ell", [(5, 6), (18, 2), (27, 1)])
+def test_blind_rotate_generic_gadgets(logL, ell):
+    """Gadgets outside the kernel's packed-digit form (logL > 16 or ell > 4: the u64 digit path)
+    and a single digit (odd ell), Tiny ring with ternary u, bit-exact with the oracle."""
+    cfg = dict(synth.load_config("tiny"), logL_rgsw=logL, ell_rgsw=ell, lwe_key="ternary", n=8,
+               name="tiny_g%d" % logL)
+    orc = Oracle(cfg)
+    K = orc.keys(cfg["seeds"]["keys"])
+    ctx = Context(cfg, 0)
+    brk = ctx.key_import(KEY_BRK, T(K["brk"].reshape(-1)))
+    rng = np.random.default_rng(logL)
+    N, n = cfg["N"], cfg["n"]
+    acc = rng.integers(0, cfg["Q"], (3, 2, N), dtype=np.uint64)
+    abar = rng.integers(0, 2 * N, (3, n)).astype(np.uint32)
+    got = H(ctx.blind_rotate(brk, T(acc), T(abar)))
+    for i in range(3):
+        assert np.array_equal(got[i], orc.blind_rotate(K["brk"], acc[i], abar[i])), i
+
+
 # ----------------------------------------------------------------------------- bootstrap
 @pytest.mark.parametrize("B", [1, 5, 16])
 def test_bootstrap_tiny_bit_exact(B):
