@@ -125,6 +125,21 @@ def test_sample_extract_all_k():
         assert np.array_equal(got[i], orc.sample_extract(ct[i], int(k)))
 
 
+def test_sample_extract_invalid_k_flagged():
+    """k outside 1..N: a zero row and the device status flag (include/fdfb.h), valid rows exact."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    N = cfg["N"]
+    ct = np.random.default_rng(6).integers(0, cfg["Q"], (4, 2, N), dtype=np.uint64)
+    ks = np.array([0, 1, N + 1, N], dtype=np.uint32)
+    got = H(ctx.sample_extract(T(ct), T(ks)))
+    with pytest.raises(Exception):
+        ctx.device_status()
+    assert not got[0].any() and not got[2].any()
+    assert np.array_equal(got[1], orc.sample_extract(ct[1], 1))
+    assert np.array_equal(got[3], orc.sample_extract(ct[3], N))
+    ctx.device_status()                                            # cleared by the read
+
+
 @pytest.mark.parametrize("name", ["tiny", "large"])
 def test_lwe_keyswitch(name):
     cfg, orc, K, ctx, dk = setup(name)
@@ -476,6 +491,28 @@ def test_permute_bit_exact(name):
     ph = orc.rlwe_phase(S, got[3])                       # decrypts to the permuted message
     e = (ph.astype(object) - msg[3][perms[3] - 1].astype(object)) % cfg["Q"]
     assert max(min(int(x), cfg["Q"] - int(x)) for x in e) < cfg["Q"] // 1024
+
+
+def test_permute_invalid_entries_are_fixed_points():
+    """A permutation entry outside 1..N is treated as a fixed point and raises the status flag
+    (include/fdfb.h): invalid entries on slots that are fixed points of a permutation give that
+    permutation's result, exactly as the oracle computes it."""
+    cfg, orc, s, S, pk, ctx, dpk = pack_setup("shift512")
+    N = cfg["N"]
+    rng = np.random.default_rng(27)
+    perm = (rng.permutation(N) + 1).astype(np.uint32)
+    for slot in (4, 101):                                           # make slots 4 and 101 fixed points
+        other = int(np.nonzero(perm == slot)[0][0])
+        perm[other], perm[slot - 1] = perm[slot - 1], slot
+    bad = perm.copy()
+    bad[[3, 100]] = [0, N + 7]                                      # invalid entries -> treated as fixed
+    ref_perm = perm
+    msg = synth.rlwe_messages(cfg, 1, seed=28)
+    ct = orc.rlwe_encrypt(29, S, msg)
+    got = H(ctx.permute(dpk, T(ct), T(bad[None])))
+    with pytest.raises(Exception):
+        ctx.device_status()
+    assert np.array_equal(got[0], orc.permute(pk, ct[0], ref_perm))
 
 
 def test_bootstrap_host_buffers_api():
