@@ -34,6 +34,12 @@ IMAD_PER_SM_CLK = 64
 # 6 IMAD.WIDE (2 slots each) + 4 IMAD (1 slot) = 16 (SASS of tools/intbench.cu k_shoup64,
 # whose measured rate, 4 modmul/SM/clk at nominal clock, confirms it).
 IMAD_PER_MODMUL = 16
+
+
+def imad_per_modmul(cfg):
+    """Slots of one direct lazy Shoup modmul at the configuration's word size: 16 for a 54-bit
+    Q (above), 4 for Q < 2^32 (IMAD.HI + 2 IMAD on 32-bit words)."""
+    return IMAD_PER_MODMUL if cfg["Q"] >= (1 << 32) else 4
 # DRAM traffic of k_blind_rotate<2048,3> per wave of 296 resident accumulators (2 per SM), from
 # `ncu --set full` (dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/ncu_full_blind_rotate.txt):
 # the RNS brK (0.81 GB) streams about twice per wave; the kernel is integer-pipe bound.
@@ -254,7 +260,7 @@ class BootstrapWorkload:
     def roofline(self, kernel_ms_per_step, ms_step):
         per_cmux, cmux_per_bs = algorithmic_work(self.cfg)
         modmul_step = per_cmux * cmux_per_bs * self.B
-        imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
+        imad_s = modmul_step * imad_per_modmul(self.cfg) / (kernel_ms_per_step / 1e3)
         peak = 148 * IMAD_PER_SM_CLK * 1965e6
         waves = self.B * (self.cfg["ell_boot"] + 1) / 296.0
         return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
@@ -262,10 +268,10 @@ class BootstrapWorkload:
                 "traffic": BR_DRAM_BYTES_PER_WAVE * waves,
                 "traffic_basis": "ncu dram bytes of one 296-accumulator wave x waves per step "
                                  "(brK re-streamed per wave; 0.2% of HBM bandwidth, not the bound)",
-                "modmul_per_step": modmul_step, "imad_per_modmul": IMAD_PER_MODMUL,
+                "modmul_per_step": modmul_step, "imad_per_modmul": imad_per_modmul(self.cfg),
                 "modmul_per_s": modmul_step / (kernel_ms_per_step / 1e3),
                 "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; "
-                              "16 slots per 54-bit Shoup modmul"}
+                              "16 slots per 54-bit Shoup modmul (4 for Q < 2^32)"}
 
     def config(self):
         cfg = self.cfg
@@ -427,7 +433,7 @@ class MultiLutWorkload(BootstrapWorkload):
         per_cmux, _ = algorithmic_work(self.cfg)
         n, u = self.cfg["n"], 2 if self.cfg["lwe_key"] == "ternary" else 1
         modmul_step = per_cmux * n * u * self.B * (self.cfg["ell_boot"] + self.k)   # ell_boot + k rotations
-        imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
+        imad_s = modmul_step * imad_per_modmul(self.cfg) / (kernel_ms_per_step / 1e3)
         peak = 148 * IMAD_PER_SM_CLK * 1965e6
         return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
                 "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None,
@@ -464,7 +470,7 @@ class TfheWorkload(BootstrapWorkload):
         per_cmux, _ = algorithmic_work(self.cfg)
         n, u = self.cfg["n"], 2 if self.cfg["lwe_key"] == "ternary" else 1
         modmul_step = per_cmux * n * u * self.B
-        imad_s = modmul_step * IMAD_PER_MODMUL / (kernel_ms_per_step / 1e3)
+        imad_s = modmul_step * imad_per_modmul(self.cfg) / (kernel_ms_per_step / 1e3)
         peak = 148 * IMAD_PER_SM_CLK * 1965e6
         return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
                 "unit": "T IMAD-slots/s", "frac": imad_s / peak, "traffic": None}
