@@ -198,15 +198,17 @@ static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, in
   if (n_acc <= 0) return FDFB_OK;
   if (abar_rows <= 0) abar_rows = (n_acc + acc_per_ct - 1) / acc_per_ct;
   const u32* k = (const u32*)bsk;
-  const bool three = c->rns.np == 3;
+  const int np = c->rns.np;
   const int s0 = gin ? s_begin : 0;
 #define BR_CASE(NN)                                                                                          \
   case NN:                                                                                                   \
     if (gin)                                                                                                 \
-      return three ? launch_br_t<NN, 3, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st) \
-                   : launch_br_t<NN, 2, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st); \
-    return three ? launch_br_t<NN, 3, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st)  \
-                 : launch_br_t<NN, 2, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st);
+      return np == 3 ? launch_br_t<NN, 3, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st) \
+           : np == 2 ? launch_br_t<NN, 2, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st) \
+                     : launch_br_t<NN, 1, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st); \
+    return np == 3 ? launch_br_t<NN, 3, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st)  \
+         : np == 2 ? launch_br_t<NN, 2, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st)  \
+                   : launch_br_t<NN, 1, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st);
   switch (c->prm.N) {
     BR_CASE(256)
     BR_CASE(512)
@@ -398,15 +400,23 @@ static int setup_rns(fdfb_ctx* c) {
   const u128 bound = (u128)(2 * p.ell_rgsw) * N * ((1ULL << p.logL_rgsw) - 1) * (p.Q - 1);
   std::vector<u64> primes;
   u128 P = 1;
-  for (u64 cand = ((1ULL << 28) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 27) && primes.size() < RNS_MAXP;
-       cand -= 2 * (u64)N) {
-    if (cand >= (1ULL << 28) || cand == p.Q || !h_is_prime(cand)) continue;
-    primes.push_back(cand);
-    P *= cand;
-    if (primes.size() >= 2 && P / 8 * 3 > bound + 1) break;
+  if (p.Q < (1ULL << 28)) {
+    // Q itself fits the 32-bit lazy butterflies (16Q < 2^32) and is NTT-friendly: one "RNS"
+    // prime p = Q computes the ring products directly mod Q (the CRT below degenerates to
+    // t_0 = r_0, P mod Q = 0), half the transforms of a 2-prime exact evaluation.
+    primes.push_back(p.Q);
+    P = p.Q;
+  } else {
+    for (u64 cand = ((1ULL << 28) - 1) / (2 * N) * (2 * N) + 1; cand > (1ULL << 27) && primes.size() < RNS_MAXP;
+         cand -= 2 * (u64)N) {
+      if (cand >= (1ULL << 28) || cand == p.Q || !h_is_prime(cand)) continue;
+      primes.push_back(cand);
+      P *= cand;
+      if (primes.size() >= 2 && P / 8 * 3 > bound + 1) break;
+    }
+    // |V| <= bound < 3P/8 keeps sum_i t_i / p_i within 1/8 of an integer (the kernel's CRT rounding)
+    if (primes.size() < 2 || P / 8 * 3 <= bound + 1) return FDFB_E_UNSUPPORTED;
   }
-  // |V| <= bound < 3P/8 keeps sum_i t_i / p_i within 1/8 of an integer (the kernel's CRT rounding)
-  if (primes.size() < 2 || P / 8 * 3 <= bound + 1) return FDFB_E_UNSUPPORTED;
   R.np = (int)primes.size();
   const u64 Q = p.Q;
   std::vector<u32> ft, it;
