@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -37,6 +38,7 @@ struct fdfb_ctx {
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
   mutable std::mutex lt_mu;
   mutable cublasLtHandle_t lt = nullptr;   // Shift-as-GEMM (int8 tensor-core GEMM, created lazily)
+  int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 never, 1 small batches (default), 2 always (NP > 1)
 };
 
 // Bracket one launch of kernel class `cls` with events on its stream when timing is on.
@@ -173,6 +175,40 @@ static int launch_ntt_batch(const fdfb_ctx* c, u64* data, size_t count, int mode
   return FDFB_OK;
 }
 
+// co-resident clusters of k_blind_rotate_cl (clusters must fit a GPC: fewer than num_sms / NP)
+template <int N, int NP>
+static int br_cluster_slots(const fdfb_ctx* c) {
+  const size_t sm = 82 * (size_t)N;
+  cudaFuncSetAttribute(k_blind_rotate_cl<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(NP * c->num_sms);
+  cfg.blockDim = dim3(N / 8);
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = NP; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int num = 0;
+  if (cudaOccupancyMaxActiveClusters(&num, k_blind_rotate_cl<N, NP>, &cfg) != cudaSuccess || num < 1) {
+    cudaGetLastError();
+    num = c->num_sms / NP;
+  }
+  return num;
+}
+
+template <int N, int NP>
+static int launch_br_cl_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
+                          const u32* abar, cudaStream_t st) {
+  constexpr int T = N / 8;
+  const size_t sm = 82 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange buffers 18N + 2 CRT slots 32N
+  cudaFuncSetAttribute(k_blind_rotate_cl<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
+  k_blind_rotate_cl<N, NP><<<NP * n_acc, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar);
+  CKL(c);
+  return FDFB_OK;
+}
+
 template <int N, int NP, bool GIN>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
                        const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
@@ -199,6 +235,35 @@ static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, in
   if (abar_rows <= 0) abar_rows = (n_acc + acc_per_ct - 1) / acc_per_ct;
   const u32* k = (const u32*)bsk;
   const int np = c->rns.np;
+  // small batches: one cluster of np CTAs per accumulator (one prime each, one CTA per SM),
+  // same arithmetic.  Measured at N = 2048, np = 3 (profiles/r01/latency): a wave of clusters
+  // takes ~27 ms, the batched kernel ~62 ms with at most one CTA per SM and ~103 ms per full
+  // wave; clusters are used when the batched kernel would run one CTA per SM and at most two
+  // waves of clusters cover the accumulators (np = 2: one wave).
+  int slots = c->num_sms / np;
+  if (np > 1 && !gin && c->br_cluster == 1) {
+    switch (c->prm.N) {
+      case 256: slots = np == 3 ? br_cluster_slots<256, 3>(c) : br_cluster_slots<256, 2>(c); break;
+      case 512: slots = np == 3 ? br_cluster_slots<512, 3>(c) : br_cluster_slots<512, 2>(c); break;
+      case 1024: slots = np == 3 ? br_cluster_slots<1024, 3>(c) : br_cluster_slots<1024, 2>(c); break;
+      default: slots = np == 3 ? br_cluster_slots<2048, 3>(c) : br_cluster_slots<2048, 2>(c); break;
+    }
+  }
+  const long cl_waves = ((long)n_acc + slots - 1) / slots;
+  const bool small = n_acc <= c->num_sms && cl_waves <= (np == 3 ? 2 : 1);
+  if (!gin && np > 1 && (c->br_cluster == 2 || (c->br_cluster == 1 && small))) {
+#define BRC_CASE(NN)                                                                                   \
+  case NN:                                                                                             \
+    return np == 3 ? launch_br_cl_t<NN, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st)          \
+                   : launch_br_cl_t<NN, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st);
+    switch (c->prm.N) {
+      BRC_CASE(256)
+      BRC_CASE(512)
+      BRC_CASE(1024)
+      BRC_CASE(2048)
+    }
+#undef BRC_CASE
+  }
   const int s0 = gin ? s_begin : 0;
 #define BR_CASE(NN)                                                                                          \
   case NN:                                                                                                   \
@@ -502,6 +567,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   CK(cudaMemset(c->d_status, 0, sizeof(int)));
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
   if ((rc = setup_rns(c))) { delete c; return rc; }
+  if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));
   d.Q = Q; d.Q2 = 2 * Q; d.Q4 = 4 * Q; d.half = (Q + 1) / 2;

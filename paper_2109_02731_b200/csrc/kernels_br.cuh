@@ -23,6 +23,7 @@
 // make_rns_tables), 8 pairs per group (7 used) -> one base per pass, 16-byte loads.
 // brK device format: [n*u steps][NP primes][2 ell rows][2 cols][N slots] u32.
 #pragma once
+#include <cooperative_groups.h>
 #include "kernels_core.cuh"
 
 #define RNS_MAXP 3
@@ -496,6 +497,148 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
     for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
   }
+}
+
+// Latency variant for small batches: a cluster of NP CTAs per accumulator, CTA rank r of the
+// cluster evaluating prime p_r only.  Every CTA keeps its own copy of acc and computes d; after
+// its inverse transform it publishes t_r (P/p_r) mod Q (< 2Q) with floor(16 t_r / p_r) in bits
+// 58..63 to a shared-memory slot, the cluster barrier makes all NP slots visible, and each CTA
+// sums them through distributed shared memory and applies the same rounding, so the copies
+// of acc stay identical (the same arithmetic as k_blind_rotate, one third of the transforms
+// per CTA).  The slots are double-buffered: one cluster barrier per CMux step.
+template <int N, int NP>
+__global__ void __cluster_dims__(NP, 1, 1) __launch_bounds__(N / 8, 1)
+k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
+                  int acc_per_ct, int abar_rows, const u32* __restrict__ abar) {
+  namespace cg = cooperative_groups;
+  using S = BrShape<N>;
+  constexpr int T = S::T;
+  cg::cluster_group cl = cg::this_cluster();
+  const int pi = (int)cl.block_rank();       // this CTA's prime
+  const int g = blockIdx.x / NP;             // accumulator (grid = NP * n_acc exactly)
+  extern __shared__ u64 smem[];
+  u64* sacc = smem;                          // [b | a], canonical mod Q (a full copy per CTA)
+  u64* sd = smem + 2 * N;                    // d, both halves
+  u32* sbuf = (u32*)(smem + 4 * N);          // 2 exchange buffers (as k_blind_rotate)
+  u64* xt = smem + 4 * N + (2 * 2 * Lay<N>::WORDS) / 2;   // 2 x [2][N] CRT-term slots
+  const int tid = threadIdx.x;
+  const u64 Q = p.Q;
+  const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
+  const u32 dmask = (1u << logL) - 1;
+  const size_t prime_words = (size_t)2 * ell * 2 * N;
+  const size_t step_words = (size_t)NP * prime_words;
+  const u32 pr = R.p[pi], pr2 = R.p2[pi];
+  const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
+  const uint4* it = R.itab + (size_t)pi * S::GROUPS * 4;
+  u64* acc = accs + (size_t)g * 2 * N;
+#pragma unroll
+  for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
+  const u32* ab = abar + (size_t)((g / acc_per_ct) % abar_rows) * p.n;
+  int buf = 0;
+#pragma unroll 1
+  for (int i = 0; i < p.n; i++) {
+    const u32 ai = __ldg(ab + i);
+#pragma unroll 1
+    for (int j = 0; j < u; j++) {
+      const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
+      const u32* K = bsk + ((size_t)i * u + j) * step_words + (size_t)pi * prime_words + 8 * tid;
+      int xb = 0;
+      __syncthreads();                           // acc of the previous step complete
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+        const u64* src = sacc + half * N;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int pos = tid + T * k;
+          const int idx = (pos - e) & (2 * N - 1);
+          const u64 v = src[idx & (N - 1)];
+          const u64 rv = (idx >= N && v) ? Q - v : v;
+          sd[half * N + pos] = sub_mod(rv, src[pos], Q);
+        }
+      }
+      u64 mb[8], ma[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
+#pragma unroll 1
+      for (int half = 0; half < 2; half++) {
+        const u64* sdh = sd + half * N;
+#pragma unroll 1
+        for (int r = 0; r < ell; r += 2) {
+          const bool two = r + 1 < ell;
+          const u32* Kb0 = K + (size_t)((half * ell + r) * 2) * N;
+          const u32* Kb1 = Kb0 + 2 * N;
+          u32 x[2][8];
+          const int sh = r * logL;
+#pragma unroll
+          for (int k = 0; k < 8; k++) {
+            const u64 dv = sdh[tid + T * k];
+            x[0][k] = (u32)(dv >> sh) & dmask;
+            x[1][k] = two ? (u32)(dv >> (sh + logL)) & dmask : 0u;
+          }
+          ntt_fwd32<N, 2>(x, sbuf + xb * 2 * Lay<N>::WORDS, tid, ft, pr, pr2, R.zero);
+          xb ^= 1;
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            if (v == 1 && !two) break;
+            const u32* Kb = v ? Kb1 : Kb0;
+            const u32* Ka = Kb + N;
+            const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
+            const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
+            const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
+            const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              mb[k] += (u64)x[v][k] * kb[k];
+              ma[k] += (u64)x[v][k] * ka[k];
+            }
+          }
+        }
+      }
+      u32 x[2][8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) { x[0][k] = redc64(mb[k], R, pi); x[1][k] = redc64(ma[k], R, pi); }
+      ntt_inv32<N, 2>(x, sbuf + xb * 2 * Lay<N>::WORDS, tid, it, pr, pr2, R.zero);
+      u64* mine = xt + (size_t)buf * 2 * N;
+#pragma unroll
+      for (int c = 0; c < 2; c++)
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int pos = tid + T * k;
+          const u32 t = csub32(x[c][k], pr);
+          const u32 f = __umulhi(t, R.f16[pi]);
+          mine[c * N + pos] = shoup64_28(t, R.M[pi], R.Ms32[pi], Q) | ((u64)f << 58);
+        }
+      cl.sync();                                   // all NP terms published
+#pragma unroll
+      for (int c = 0; c < 2; c++)
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int pos = tid + T * k;
+          u64 a = sacc[c * N + pos];
+          u32 F = 0;
+#pragma unroll
+          for (int r2 = 0; r2 < NP; r2++) {
+            const u64* other = cl.map_shared_rank(xt + (size_t)buf * 2 * N, r2);
+            const u64 v = other[c * N + pos];
+            a += v & ((1ull << 58) - 1);
+            F += (u32)(v >> 58);
+          }
+          const u32 kk = (F + 8) >> 4;                                  // round(sum t_r / p_r)
+          a += (u64)(NP + 1) * Q - (u64)kk * R.pq;                      // < 11Q
+          a = csub(a, Q << 3);
+          a = csub(a, Q << 2);
+          a = csub(a, Q << 1);
+          sacc[c * N + pos] = csub(a, Q);
+        }
+      buf ^= 1;
+    }
+  }
+  __syncthreads();
+  if (pi == 0) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
+  }
+  cl.sync();                                       // no CTA leaves while its slots may be read
 }
 
 // brK import: canonical RGSW rows (coefficient domain, [0, Q)) -> for each prime p_i:

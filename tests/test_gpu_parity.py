@@ -193,6 +193,24 @@ def test_blind_rotate_generic_gadgets(logL, ell):
         assert np.array_equal(got[i], orc.blind_rotate(K["brk"], acc[i], abar[i])), i
 
 
+@pytest.mark.parametrize("name", ["fhew", "large"])
+def test_blind_rotate_cluster_path_equals_batched_kernel(name, monkeypatch):
+    """The small-batch cluster kernel (one RNS prime per CTA, CRT terms combined through
+    distributed shared memory) gives the batched kernel's bytes; both are pinned to the oracle
+    elsewhere (the FHEW-like parity tests run on the cluster path)."""
+    cfg = synth.load_config(name)
+    outs = []
+    for mode in ("0", "2"):
+        monkeypatch.setenv("FDFB_BR_CLUSTER", mode)
+        ctx = Context(cfg, 0)
+        keys = ctx.keygen(cfg["seeds"]["keys"], which=0x03)
+        g = torch.Generator(device="cuda").manual_seed(3)
+        acc = torch.randint(0, cfg["Q"], (5, 2, cfg["N"]), device="cuda", generator=g).to(torch.uint64)
+        abar = torch.randint(0, 2 * cfg["N"], (5, cfg["n"]), device="cuda", generator=g).to(torch.uint32)
+        outs.append(H(ctx.blind_rotate(keys["brk"], acc, abar)))
+    assert np.array_equal(outs[0], outs[1])
+
+
 # ----------------------------------------------------------------------------- bootstrap
 @pytest.mark.parametrize("B", [1, 5, 16])
 def test_bootstrap_tiny_bit_exact(B):
