@@ -193,12 +193,12 @@ def test_blind_rotate_generic_gadgets(logL, ell):
         assert np.array_equal(got[i], orc.blind_rotate(K["brk"], acc[i], abar[i])), i
 
 
-@pytest.mark.parametrize("name", ["fhew", "large"])
+@pytest.mark.parametrize("name", ["fhew", "large", "shift512"])
 def test_blind_rotate_cluster_path_equals_batched_kernel(name, monkeypatch):
     """The small-batch cluster kernel (one RNS prime per CTA, CRT terms combined through
     distributed shared memory) gives the batched kernel's bytes; both are pinned to the oracle
     elsewhere (the FHEW-like parity tests run on the cluster path)."""
-    cfg = synth.load_config(name)
+    cfg = SHIFT512 if name == "shift512" else synth.load_config(name)   # N = 512 with 3 primes
     outs = []
     for mode in ("0", "2"):
         monkeypatch.setenv("FDFB_BR_CLUSTER", mode)
