@@ -38,7 +38,7 @@ struct fdfb_ctx {
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
   mutable std::mutex lt_mu;
   mutable cublasLtHandle_t lt = nullptr;   // Shift-as-GEMM (int8 tensor-core GEMM, created lazily)
-  int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 never, 1 small batches (default), 2 always (NP > 1)
+  int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 batched only, 1 auto (default), 2 / 3 force clusters of NP / 2 NP
 };
 
 // Bracket one launch of kernel class `cls` with events on its stream when timing is on.
@@ -175,37 +175,63 @@ static int launch_ntt_batch(const fdfb_ctx* c, u64* data, size_t count, int mode
   return FDFB_OK;
 }
 
-// co-resident clusters of k_blind_rotate_cl (clusters must fit a GPC: fewer than num_sms / NP)
-template <int N, int NP>
+// co-resident clusters of k_blind_rotate_cl (a cluster must fit a GPC, so fewer than
+// num_sms / (NP SPLIT) in general)
+template <int N, int NP, int SPLIT>
 static int br_cluster_slots(const fdfb_ctx* c) {
-  const size_t sm = 82 * (size_t)N;
-  cudaFuncSetAttribute(k_blind_rotate_cl<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const size_t sm = 66 * (size_t)N;
+  cudaFuncSetAttribute(k_blind_rotate_cl<N, NP, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(NP * c->num_sms);
+  cfg.gridDim = dim3(NP * SPLIT * c->num_sms);
   cfg.blockDim = dim3(N / 8);
   cfg.dynamicSmemBytes = sm;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = NP; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  attr.val.clusterDim.x = NP * SPLIT; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   int num = 0;
-  if (cudaOccupancyMaxActiveClusters(&num, k_blind_rotate_cl<N, NP>, &cfg) != cudaSuccess || num < 1) {
+  if (cudaOccupancyMaxActiveClusters(&num, k_blind_rotate_cl<N, NP, SPLIT>, &cfg) != cudaSuccess || num < 1) {
     cudaGetLastError();
-    num = c->num_sms / NP;
+    num = c->num_sms / (NP * SPLIT);
   }
   return num;
 }
 
-template <int N, int NP>
+template <int N, int NP, int SPLIT>
 static int launch_br_cl_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
                           const u32* abar, cudaStream_t st) {
   constexpr int T = N / 8;
-  const size_t sm = 82 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange buffers 18N + 2 CRT slots 32N
-  cudaFuncSetAttribute(k_blind_rotate_cl<N, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const size_t sm = 66 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange buffers 18N + 2 residue slots 16N
+  cudaFuncSetAttribute(k_blind_rotate_cl<N, NP, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
-  k_blind_rotate_cl<N, NP><<<NP * n_acc, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar);
+  k_blind_rotate_cl<N, NP, SPLIT><<<NP * SPLIT * n_acc, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct,
+                                                                       abar_rows, abar);
   CKL(c);
+  return FDFB_OK;
+}
+
+// small-batch path selection: 0 = batched kernel, 1 = clusters of NP, 2 = clusters of 2 NP
+template <int N, int NP>
+static int br_cluster_choice(const fdfb_ctx* c, int n_acc) {
+  if (c->br_cluster == 0) return 0;
+  if (c->br_cluster == 2) return 1;
+  if (c->br_cluster == 3) return 2;
+  if (n_acc > c->num_sms) return 0;
+  if (n_acc <= br_cluster_slots<N, NP, 2>(c)) return 2;                  // one wave of split clusters
+  const int slots = br_cluster_slots<N, NP, 1>(c);
+  return n_acc <= (NP == 3 ? 2 : 1) * slots ? 1 : 0;
+}
+
+template <int N, int NP>
+static int launch_br_small(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
+                           const u32* abar, cudaStream_t st, bool* done) {
+  *done = true;
+  switch (br_cluster_choice<N, NP>(c, n_acc)) {
+    case 2: return launch_br_cl_t<N, NP, 2>(c, bsk, accs, n_acc, acc_per_ct, abar_rows, abar, st);
+    case 1: return launch_br_cl_t<N, NP, 1>(c, bsk, accs, n_acc, acc_per_ct, abar_rows, abar, st);
+  }
+  *done = false;
   return FDFB_OK;
 }
 
@@ -235,34 +261,25 @@ static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, in
   if (abar_rows <= 0) abar_rows = (n_acc + acc_per_ct - 1) / acc_per_ct;
   const u32* k = (const u32*)bsk;
   const int np = c->rns.np;
-  // small batches: one cluster of np CTAs per accumulator (one prime each, one CTA per SM),
-  // same arithmetic.  Measured at N = 2048, np = 3 (profiles/r01/latency): a wave of clusters
-  // takes ~27 ms, the batched kernel ~62 ms with at most one CTA per SM and ~103 ms per full
-  // wave; clusters are used when the batched kernel would run one CTA per SM and at most two
-  // waves of clusters cover the accumulators (np = 2: one wave).
-  int slots = c->num_sms / np;
-  if (np > 1 && !gin && c->br_cluster == 1) {
+  // small passes: clusters of np (or 2 np) CTAs per accumulator, one RNS prime (and one d half)
+  // per CTA, same arithmetic (k_blind_rotate_cl).  Measured at N = 2048, np = 3
+  // (profiles/r01/latency): chosen when the batched kernel would run one CTA per SM and the
+  // clusters need at most two waves (np = 2: one); FDFB_BR_CLUSTER = 0 / 2 / 3 forces batched /
+  // clusters of np / clusters of 2 np.
+  if (!gin && np > 1) {
+    bool done = false;
+    int rc = FDFB_OK;
     switch (c->prm.N) {
-      case 256: slots = np == 3 ? br_cluster_slots<256, 3>(c) : br_cluster_slots<256, 2>(c); break;
-      case 512: slots = np == 3 ? br_cluster_slots<512, 3>(c) : br_cluster_slots<512, 2>(c); break;
-      case 1024: slots = np == 3 ? br_cluster_slots<1024, 3>(c) : br_cluster_slots<1024, 2>(c); break;
-      default: slots = np == 3 ? br_cluster_slots<2048, 3>(c) : br_cluster_slots<2048, 2>(c); break;
+      case 256: rc = np == 3 ? launch_br_small<256, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done)
+                             : launch_br_small<256, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done); break;
+      case 512: rc = np == 3 ? launch_br_small<512, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done)
+                             : launch_br_small<512, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done); break;
+      case 1024: rc = np == 3 ? launch_br_small<1024, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done)
+                              : launch_br_small<1024, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done); break;
+      case 2048: rc = np == 3 ? launch_br_small<2048, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done)
+                              : launch_br_small<2048, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st, &done); break;
     }
-  }
-  const long cl_waves = ((long)n_acc + slots - 1) / slots;
-  const bool small = n_acc <= c->num_sms && cl_waves <= (np == 3 ? 2 : 1);
-  if (!gin && np > 1 && (c->br_cluster == 2 || (c->br_cluster == 1 && small))) {
-#define BRC_CASE(NN)                                                                                   \
-  case NN:                                                                                             \
-    return np == 3 ? launch_br_cl_t<NN, 3>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st)          \
-                   : launch_br_cl_t<NN, 2>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, st);
-    switch (c->prm.N) {
-      BRC_CASE(256)
-      BRC_CASE(512)
-      BRC_CASE(1024)
-      BRC_CASE(2048)
-    }
-#undef BRC_CASE
+    if (done) return rc;
   }
   const int s0 = gin ? s_begin : 0;
 #define BR_CASE(NN)                                                                                          \

@@ -499,28 +499,31 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
   }
 }
 
-// Latency variant for small batches: a cluster of NP CTAs per accumulator, CTA rank r of the
-// cluster evaluating prime p_r only.  Every CTA keeps its own copy of acc and computes d; after
-// its inverse transform it publishes t_r (P/p_r) mod Q (< 2Q) with floor(16 t_r / p_r) in bits
-// 58..63 to a shared-memory slot, the cluster barrier makes all NP slots visible, and each CTA
-// sums them through distributed shared memory and applies the same rounding, so the copies
-// of acc stay identical (the same arithmetic as k_blind_rotate, one third of the transforms
-// per CTA).  The slots are double-buffered: one cluster barrier per CMux step.
-template <int N, int NP>
-__global__ void __cluster_dims__(NP, 1, 1) __launch_bounds__(N / 8, 1)
+// Latency variant for small batches: a cluster of NP x SPLIT CTAs per accumulator.  CTA rank
+// (prime pi, part sp) evaluates prime p_pi only, and with SPLIT = 2 only the digit pairs of
+// half sp (its own d half): its transforms, MAC and inverse transform give the partial
+// residue t^(sp) = r^(sp) y_pi mod p_pi of both output columns, published to a double-buffered
+// shared-memory slot.  One cluster barrier per CMux makes all slots visible; every CTA reads
+// them through distributed shared memory, sums the parts per prime mod p, and applies the
+// batched kernel's CRT (terms t (P/p) mod Q, rounding from floor(16 t / p)), so the copies of
+// acc in the cluster stay identical and the result is bit-identical to k_blind_rotate.
+template <int N, int NP, int SPLIT>
+__global__ void __cluster_dims__(NP * SPLIT, 1, 1) __launch_bounds__(N / 8, 1)
 k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
                   int acc_per_ct, int abar_rows, const u32* __restrict__ abar) {
   namespace cg = cooperative_groups;
   using S = BrShape<N>;
   constexpr int T = S::T;
+  constexpr int CL = NP * SPLIT;
   cg::cluster_group cl = cg::this_cluster();
-  const int pi = (int)cl.block_rank();       // this CTA's prime
-  const int g = blockIdx.x / NP;             // accumulator (grid = NP * n_acc exactly)
+  const int rank = (int)cl.block_rank();
+  const int pi = rank / SPLIT, sp = rank % SPLIT;     // prime, part (SPLIT = 2: the d half)
+  const int g = blockIdx.x / CL;                      // accumulator (grid = CL * n_acc exactly)
   extern __shared__ u64 smem[];
-  u64* sacc = smem;                          // [b | a], canonical mod Q (a full copy per CTA)
-  u64* sd = smem + 2 * N;                    // d, both halves
-  u32* sbuf = (u32*)(smem + 4 * N);          // 2 exchange buffers (as k_blind_rotate)
-  u64* xt = smem + 4 * N + (2 * 2 * Lay<N>::WORDS) / 2;   // 2 x [2][N] CRT-term slots
+  u64* sacc = smem;                                   // [b | a], canonical mod Q (a copy per CTA)
+  u64* sd = smem + 2 * N;                             // d, both halves
+  u32* sbuf = (u32*)(smem + 4 * N);                   // 2 exchange buffers (as k_blind_rotate)
+  u32* slot = sbuf + 4 * Lay<N>::WORDS;               // 2 x [2][N] partial residues
   const int tid = threadIdx.x;
   const u64 Q = p.Q;
   const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
@@ -530,6 +533,7 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
   const u32 pr = R.p[pi], pr2 = R.p2[pi];
   const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
   const uint4* it = R.itab + (size_t)pi * S::GROUPS * 4;
+  const int h0 = SPLIT == 2 ? sp : 0, h1 = SPLIT == 2 ? sp + 1 : 2;   // halves of this CTA
   u64* acc = accs + (size_t)g * 2 * N;
 #pragma unroll
   for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
@@ -543,9 +547,9 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
       const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
       const u32* K = bsk + ((size_t)i * u + j) * step_words + (size_t)pi * prime_words + 8 * tid;
       int xb = 0;
-      __syncthreads();                           // acc of the previous step complete
-#pragma unroll
-      for (int half = 0; half < 2; half++) {
+      __syncthreads();                                // acc of the previous step complete
+#pragma unroll 1
+      for (int half = h0; half < h1; half++) {
         const u64* src = sacc + half * N;
 #pragma unroll
         for (int k = 0; k < 8; k++) {
@@ -560,7 +564,7 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
 #pragma unroll
       for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
 #pragma unroll 1
-      for (int half = 0; half < 2; half++) {
+      for (int half = h0; half < h1; half++) {
         const u64* sdh = sd + half * N;
 #pragma unroll 1
         for (int r = 0; r < ell; r += 2) {
@@ -598,17 +602,15 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
 #pragma unroll
       for (int k = 0; k < 8; k++) { x[0][k] = redc64(mb[k], R, pi); x[1][k] = redc64(ma[k], R, pi); }
       ntt_inv32<N, 2>(x, sbuf + xb * 2 * Lay<N>::WORDS, tid, it, pr, pr2, R.zero);
-      u64* mine = xt + (size_t)buf * 2 * N;
+      u32* mine = slot + (size_t)buf * 2 * N;
 #pragma unroll
       for (int c = 0; c < 2; c++)
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const int pos = tid + T * k;
-          const u32 t = csub32(x[c][k], pr);
-          const u32 f = __umulhi(t, R.f16[pi]);
-          mine[c * N + pos] = shoup64_28(t, R.M[pi], R.Ms32[pi], Q) | ((u64)f << 58);
-        }
-      cl.sync();                                   // all NP terms published
+        for (int k = 0; k < 8; k++) mine[c * N + tid + T * k] = csub32(x[c][k], pr);   // t^(sp) in [0, p)
+      cl.sync();                                      // all CL partial residues published
+      const u32* sl[CL];
+#pragma unroll
+      for (int r2 = 0; r2 < CL; r2++) sl[r2] = cl.map_shared_rank(slot + (size_t)buf * 2 * N, r2);
 #pragma unroll
       for (int c = 0; c < 2; c++)
 #pragma unroll
@@ -617,13 +619,13 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
           u64 a = sacc[c * N + pos];
           u32 F = 0;
 #pragma unroll
-          for (int r2 = 0; r2 < NP; r2++) {
-            const u64* other = cl.map_shared_rank(xt + (size_t)buf * 2 * N, r2);
-            const u64 v = other[c * N + pos];
-            a += v & ((1ull << 58) - 1);
-            F += (u32)(v >> 58);
+          for (int q = 0; q < NP; q++) {
+            u32 t = sl[q * SPLIT][c * N + pos];
+            if (SPLIT == 2) t = csub32(t + sl[q * SPLIT + 1][c * N + pos], R.p[q]);
+            F += __umulhi(t, R.f16[q]);
+            a += shoup64_28(t, R.M[q], R.Ms32[q], Q);                  // < 2Q each
           }
-          const u32 kk = (F + 8) >> 4;                                  // round(sum t_r / p_r)
+          const u32 kk = (F + 8) >> 4;                                  // round(sum t_q / p_q)
           a += (u64)(NP + 1) * Q - (u64)kk * R.pq;                      // < 11Q
           a = csub(a, Q << 3);
           a = csub(a, Q << 2);
@@ -634,11 +636,11 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
     }
   }
   __syncthreads();
-  if (pi == 0) {
+  if (rank == 0) {
 #pragma unroll
     for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
   }
-  cl.sync();                                       // no CTA leaves while its slots may be read
+  cl.sync();                                          // no CTA leaves while its slots may be read
 }
 
 // brK import: canonical RGSW rows (coefficient domain, [0, Q)) -> for each prime p_i:

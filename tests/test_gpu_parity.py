@@ -200,7 +200,7 @@ def test_blind_rotate_cluster_path_equals_batched_kernel(name, monkeypatch):
     elsewhere (the FHEW-like parity tests run on the cluster path)."""
     cfg = SHIFT512 if name == "shift512" else synth.load_config(name)   # N = 512 with 3 primes
     outs = []
-    for mode in ("0", "2"):
+    for mode in ("0", "2", "3"):                                    # batched, clusters of NP, of 2 NP
         monkeypatch.setenv("FDFB_BR_CLUSTER", mode)
         ctx = Context(cfg, 0)
         keys = ctx.keygen(cfg["seeds"]["keys"], which=0x03)
@@ -208,7 +208,7 @@ def test_blind_rotate_cluster_path_equals_batched_kernel(name, monkeypatch):
         acc = torch.randint(0, cfg["Q"], (5, 2, cfg["N"]), device="cuda", generator=g).to(torch.uint64)
         abar = torch.randint(0, 2 * cfg["N"], (5, cfg["n"]), device="cuda", generator=g).to(torch.uint32)
         outs.append(H(ctx.blind_rotate(keys["brk"], acc, abar)))
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
 # ----------------------------------------------------------------------------- bootstrap
