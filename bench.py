@@ -12,6 +12,11 @@ inputs are resident in HBM when the timed region starts.  Per-GPU work is fixed
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on this box's
 host cores on a bounded sample of the same workload (rank 0 only).
+
+Other workloads (same JSON contract; not the driver's headline): --workload multilut
+(k LUTs per input), tfhe, shift, permute, shiftboot; --box runs BASELINE's Box-scale
+configuration (65536 ciphertexts sharded over the ranks, strong scaling); --config
+tiny / fhew times the parity-only parameter sets.
 """
 import argparse
 import json
