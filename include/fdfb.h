@@ -130,6 +130,18 @@ int fdfb_lwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_lwe, c
 int fdfb_rlwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_rlwe, const uint64_t* msg,
                       uint32_t count, uint64_t* out, void* stream);
 
+/* ------------------------------------------------------------------ decryption (secret-key side)
+ * Phase of LWE ciphertexts ct [dev, count x (n+1)] mod q_lwe under sk_lwe [dev, n int8]:
+ * phase[c] = b - <a, s> mod q_lwe.  With t > 0 also decoded: msg[c] =
+ * round(t phase / q_lwe) mod t (PAPER.md:1725 rounding, ties up); msg may be NULL.
+ * phase [dev, count] may be NULL when only msg is wanted. */
+int fdfb_lwe_decrypt(const fdfb_ctx* ctx, const int8_t* sk_lwe, const uint64_t* ct, uint32_t count, uint32_t t,
+                     uint64_t* phase, uint64_t* msg, void* stream);
+/* Phase of RLWE ciphertexts ct [dev, count x 2 x N] under sk_rlwe [dev, N int8]:
+ * out = b - a * s mod Q (negacyclic product) [dev, count x N]. */
+int fdfb_rlwe_phase(const fdfb_ctx* ctx, const int8_t* sk_rlwe, const uint64_t* ct, uint32_t count, uint64_t* out,
+                    void* stream);
+
 /* ------------------------------------------------------------------ LUT
  * BootsMap[x] = round(Q/t_out) * lut[x] then SetupPolynomial
  * (Fig. SetupPolynomial, half-open windows, reading F6).

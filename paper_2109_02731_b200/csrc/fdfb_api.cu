@@ -1147,6 +1147,39 @@ extern "C" int fdfb_poly_mul(const fdfb_ctx* c, const uint64_t* a, const uint64_
   return rc;
 }
 
+extern "C" int fdfb_lwe_decrypt(const fdfb_ctx* c, const int8_t* sk, const uint64_t* ct, uint32_t count, uint32_t t,
+                                uint64_t* phase, uint64_t* msg, void* stream) {
+  if (!c) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!sk || !ct || (!phase && !msg)) return FDFB_E_NULL;
+  if (msg && t == 0) return FDFB_E_PLAINTEXT;
+  const unsigned blocks = (unsigned)(((size_t)count * 32 + 255) / 256);
+  k_lwe_decrypt<<<blocks, 256, 0, S(stream)>>>(c->dp, sk, ct, (int)count, t, phase, msg);
+  CKL(c);
+  return FDFB_OK;
+}
+
+extern "C" int fdfb_rlwe_phase(const fdfb_ctx* c, const int8_t* sk, const uint64_t* ct, uint32_t count, uint64_t* out,
+                               void* stream) {
+  if (!c) return FDFB_E_NULL;
+  if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (!sk || !ct || !out) return FDFB_E_NULL;
+  cudaStream_t st = S(stream);
+  const size_t tot = (size_t)count * c->prm.N;
+  u64* buf;
+  CK(cudaMallocAsync(&buf, 3 * tot * 8, st));
+  u64 *a = buf, *sp = buf + tot, *prod = buf + 2 * tot;
+  k_rlwe_phase_prep<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct, sk, (int)count, a, sp);
+  CKL(c);
+  int rc = fdfb_poly_mul(c, a, sp, prod, count, st);
+  if (!rc) {
+    k_rlwe_phase_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct, prod, (int)count, out);
+    CKL(c);
+  }
+  cudaFreeAsync(buf, st);
+  return rc;
+}
+
 extern "C" int fdfb_cdt_table(const fdfb_ctx* c, uint64_t* thr, int* T) {
   if (!c || !T) return FDFB_E_NULL;
   *T = c->dp.cdt_T;

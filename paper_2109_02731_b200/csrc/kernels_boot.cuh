@@ -274,3 +274,45 @@ __global__ void k_shiftbr_amount(DevParams p, const u32* __restrict__ abar, int 
   const u32 v = (p.u == 2 && j == 0) ? a : ((u32)p.N - a) & (u32)(p.N - 1);
   d[c] = v ? v : 1u;
 }
+
+// ------------------------------------------------------------------ decryption helpers
+// phase = b - <a, s> mod q_lwe (one warp per ciphertext); msg = round(t phase / q) mod t.
+__global__ void k_lwe_decrypt(DevParams p, const int8_t* __restrict__ s, const u64* __restrict__ ct, int count,
+                              u32 t, u64* __restrict__ phase, u64* __restrict__ msg) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= count) return;
+  const u64* c = ct + (size_t)warp * (p.n + 1);
+  u64 acc = 0;                                      // exact mod 2^64, then mod q_lwe
+  for (int i = lane; i < p.n; i += 32) acc += c[1 + i] * (u64)(long long)s[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    const u64 ph = (c[0] - acc) & p.q_mask;
+    if (phase) phase[warp] = ph;
+    if (msg && t) {
+      const unsigned __int128 num = (unsigned __int128)ph * t * 2 + ((unsigned __int128)1 << p.log_q_lwe);
+      msg[warp] = (u64)((num >> (p.log_q_lwe + 1)) % t);
+    }
+  }
+}
+// out = b - prod (prod = a * s in coefficient form, from fdfb_poly_mul's NTT path)
+__global__ void k_rlwe_phase_finish(DevParams p, const u64* __restrict__ ct, const u64* __restrict__ prod, int count,
+                                    u64* __restrict__ out) {
+  const int N = p.N;
+  const size_t total = (size_t)count * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    const size_t c = x / N, j = x % N;
+    out[x] = sub_mod(ct[c * 2 * N + j], prod[x], p.Q);
+  }
+}
+__global__ void k_rlwe_phase_prep(DevParams p, const u64* __restrict__ ct, const int8_t* __restrict__ s, int count,
+                                  u64* __restrict__ a, u64* __restrict__ sp) {
+  const int N = p.N;
+  const size_t total = (size_t)count * N;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    const size_t c = x / N, j = x % N;
+    a[x] = ct[c * 2 * N + N + j];
+    const int v = s[j];
+    sp[x] = v >= 0 ? (u64)v : p.Q - (u64)(-v);
+  }
+}

@@ -44,7 +44,7 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming",
             "fdfb_workspace_keyswitch", "fdfb_workspace_bootstrap_multi", "fdfb_bootstrap_multi_batch",
             "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute",
-            "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch"]
+            "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch", "fdfb_lwe_decrypt", "fdfb_rlwe_phase"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -90,6 +90,8 @@ def lib():
         L.fdfb_workspace_bootstrap_shift.argtypes = [vp, u32]
         L.fdfb_workspace_bootstrap_shift.restype = sz
         L.fdfb_bootstrap_shift_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
+        L.fdfb_lwe_decrypt.argtypes = [vp, vp, vp, u32, u32, vp, vp, vp]
+        L.fdfb_rlwe_phase.argtypes = [vp, vp, vp, u32, vp, vp]
         L.fdfb_workspace_permute.argtypes = [vp, u32]
         L.fdfb_workspace_permute.restype = sz
         L.fdfb_permute.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
@@ -237,6 +239,23 @@ class Context:
         out = self._u64(msgs.numel(), self.n + 1)
         _check(lib().fdfb_lwe_encrypt(self.h, C.c_uint64(seed), _ptr(s), _ptr(msgs), msgs.numel(),
                                       1 if exact else 0, _ptr(out), _stream(stream)))
+        return out
+
+    def lwe_decrypt(self, s, ct, t=None, stream=None):
+        """Phase b - <a, s> mod q_lwe of every LWE ciphertext, and with t the decoded message
+        round(t phase / q_lwe) mod t (fdfb_lwe_decrypt).  Returns (phase, msg or None)."""
+        B = ct.shape[0]
+        phase = self._u64(B)
+        msg = self._u64(B) if t else None
+        _check(lib().fdfb_lwe_decrypt(self.h, _ptr(s), _ptr(ct), B, int(t or 0), _ptr(phase), _ptr(msg),
+                                      _stream(stream)))
+        return phase, msg
+
+    def rlwe_phase(self, S, ct, stream=None):
+        """b - a * S mod Q of every RLWE ciphertext [B, 2, N] (fdfb_rlwe_phase)."""
+        B = ct.shape[0]
+        out = self._u64(B, self.N)
+        _check(lib().fdfb_rlwe_phase(self.h, _ptr(S), _ptr(ct), B, _ptr(out), _stream(stream)))
         return out
 
     def rlwe_encrypt(self, seed, S, msgs: torch.Tensor, stream=None):

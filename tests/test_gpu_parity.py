@@ -141,6 +141,25 @@ def test_sample_extract_invalid_k_flagged():
 
 
 @pytest.mark.parametrize("name", ["tiny", "large"])
+def test_decryption_helpers_match_oracle(name):
+    """fdfb_lwe_decrypt (phase and decoded message) and fdfb_rlwe_phase vs the oracle's phase
+    definitions and decode rounding (1725)."""
+    cfg, orc, K, ctx, dk = setup(name)
+    rng = np.random.default_rng(12)
+    B, t = 37, cfg["t"]
+    cts = rng.integers(0, 1 << cfg["log_q_lwe"], (B, cfg["n"] + 1), dtype=np.uint64)
+    ph, msg = ctx.lwe_decrypt(T(K["s"]), T(cts), t=t)
+    ph, msg = H(ph), H(msg)
+    for c in range(B):
+        want = orc.lwe_phase(K["s"], cts[c])
+        assert int(ph[c]) == want and int(msg[c]) == orc.decode(want, 1 << cfg["log_q_lwe"], t), c
+    rl = rng.integers(0, cfg["Q"], (3, 2, cfg["N"]), dtype=np.uint64)
+    got = H(ctx.rlwe_phase(T(K["S"]), T(rl)))
+    for c in range(3):
+        assert np.array_equal(got[c], orc.rlwe_phase(K["S"], rl[c])), c
+
+
+@pytest.mark.parametrize("name", ["tiny", "large"])
 def test_lwe_keyswitch(name):
     cfg, orc, K, ctx, dk = setup(name)
     rng = np.random.default_rng(3)
