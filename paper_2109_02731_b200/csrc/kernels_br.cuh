@@ -14,10 +14,17 @@
 // vector as the schoolbook definition (bit-exact with any correct evaluation); it costs
 // ~4 IMAD slots per 30-bit butterfly instead of ~16-22 for a 54-bit Shoup butterfly.
 //
-// Per CMux and prime p: 2 ell forward NTT_p of the digit polynomials (registers, radix-8
-// passes, one smem exchange each, u32), lazy 64-bit MAC against the NTT_p-domain key
-// (u32, N^{-1} (P/p)^{-1} folded in), one reduction, 2 inverse NTT_p, and the prime's CRT term added
-// to acc (the rounding k = round(sum t_i / p_i) and acc -= k P mod Q after the last prime).
+// Per CMux: d once (both halves); then per prime p: 2 ell forward NTT_p of the digit
+// polynomials (pairs of digits per transform; registers, radix-8 passes, smem exchanges in
+// two alternating buffers), lazy 64-bit MAC against the NTT_p-domain key (u32, N^{-1} y_p 2^32
+// folded in), Montgomery reduction, one paired inverse NTT_p of both columns, and the prime's
+// CRT term added to acc (the rounding k = round(sum t_i / p_i) and acc -= k P mod Q after the
+// last prime).  For Q < 2^28 the single prime p = Q computes the products directly mod Q.
+//
+// Kernels: k_blind_rotate (batched: one CTA per accumulator, persistent over the batch, also
+// the shift-based BR's CMux in GIN mode) and k_blind_rotate_cl (small passes: a thread-block
+// cluster of NP or 2 NP CTAs per accumulator, one prime [and one d half] per CTA, partial
+// residues combined through distributed shared memory).
 //
 // Twiddles: pass-grouped tables of (w, w') u32 pairs per prime (fdfb_api.cu
 // make_rns_tables), 8 pairs per group (7 used) -> one base per pass, 16-byte loads.
