@@ -274,8 +274,12 @@ class BootstrapWorkload:
         imad_s = modmul_step * imad_per_modmul(self.cfg) / (kernel_ms_per_step / 1e3)
         peak = 148 * IMAD_PER_SM_CLK * 1965e6
         waves = self.B * (self.cfg["ell_boot"] + 1) / 296.0
+        hbm_peak = json.load(open(PEAKS_FILE))["hbm_gbs"] if os.path.exists(PEAKS_FILE) else 6549.8
+        hbm_gbs = BR_DRAM_BYTES_PER_WAVE * waves / (kernel_ms_per_step / 1e3) / 1e9
         return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
                 "unit": "T IMAD-slots/s", "frac": imad_s / peak,
+                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
+                        "basis": "key-stream DRAM bytes (ncu) / BR time vs MEASURED_PEAKS.json hbm_gbs"},
                 "traffic": BR_DRAM_BYTES_PER_WAVE * waves,
                 "traffic_basis": "ncu dram bytes of one 296-accumulator wave x waves per step "
                                  "(brK re-streamed per wave; 0.2% of HBM bandwidth, not the bound)",
