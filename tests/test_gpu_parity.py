@@ -462,6 +462,20 @@ def test_bootstrap_multi_lut_equals_single_lut_oracle(B):
         assert np.array_equal(got[kk], orc.bootstrap(K, rotp, cts)), kk
 
 
+def test_bootstrap_multi_lut_k1_and_ragged():
+    """k = 1 is the single-LUT bootstrap; k = 5 on a ragged batch of 3 matches per LUT."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    msgs = synth.messages(cfg, 3, seed=41)
+    cts = T(orc.lwe_encrypt(42, K["s"], msgs))
+    luts = [synth.lut(cfg, seed=70 + kk) for kk in range(5)]
+    rot = torch.stack([ctx.setup_lut(f) for f in luts])
+    one = H(ctx.bootstrap_multi(dk, rot[:1], cts))
+    assert np.array_equal(one[0], H(ctx.bootstrap_batch(dk, rot[0], cts)))
+    five = H(ctx.bootstrap_multi(dk, rot, cts))
+    for kk in range(5):
+        assert np.array_equal(five[kk], H(ctx.bootstrap_batch(dk, rot[kk], cts))), kk
+
+
 def test_bootstrap_multi_lut_large_equals_single():
     cfg, orc, K, ctx, dk = setup("large")
     luts = [synth.lut(cfg, seed=60 + kk) for kk in range(2)]
@@ -483,6 +497,24 @@ def test_bootstrap_tfhe_bit_exact(name, B):
     cts = orc.lwe_encrypt(12, K["s"], msgs)
     got = H(ctx.bootstrap_tfhe(dk, rot, T(cts)))
     assert np.array_equal(got, orc.bootstrap_tfhe(K, rotp[0], cts))
+
+
+@pytest.mark.slow
+def test_bootstrap_tfhe_large_sampled_bit_exact():
+    """TFHE bootstrap at the Large set (one blind rotation of 2048 CMux steps) for a batch of 300
+    (the batched kernel), two sampled outputs bit-exact with the oracle; and the same inputs at
+    B = 3 (the small-batch cluster path) give the same bytes."""
+    cfg, orc, K, ctx, dk = setup("large")
+    f = synth.lut(cfg, seed=19)
+    rotp = orc.setup_polynomial(orc.bootsmap(f))
+    rot = ctx.setup_lut(f)
+    msgs = synth.messages(cfg, 300, seed=20)
+    cts = orc.lwe_encrypt(21, K["s"], msgs)
+    got = H(ctx.bootstrap_tfhe(dk, rot, T(cts)))
+    small = H(ctx.bootstrap_tfhe(dk, rot, T(cts[:3])))
+    assert np.array_equal(small, got[:3])
+    for i in (0, 299):
+        assert np.array_equal(got[i], orc.bootstrap_tfhe(K, rotp[0], cts[i:i + 1])[0]), i
 
 
 def test_bootstrap_tfhe_negacyclic_contrast_large():
