@@ -101,22 +101,10 @@ FDFB_DEV void bin32(u32& X, u32& Y, u32 w, u32 ws, u32 p, u32 p2, u32 z) {   // 
 
 // 8 pairs of a group: tw[0] stage-0, tw[1..2] stage-1, tw[3..6] stage-2 (tw[7] padding)
 struct Tw8 { u32 w[8], s[8]; };
-FDFB_DEV uint4 ldg_keep(const uint4* p) {           // twiddles: reused by every transform
-  uint4 v;
-  asm("ld.global.nc.L1::evict_last.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  return v;
-}
-FDFB_DEV uint4 ldg_stream(const uint4* p) {         // brK rows: read once per CTA and step
-  uint4 v;
-  asm("ld.global.nc.L1::evict_first.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  return v;
-}
 FDFB_DEV void load_tw8(Tw8& t, const uint4* g) {
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    const uint4 v = ldg_keep(g + i);
+    const uint4 v = __ldg(g + i);
     t.w[2 * i] = v.x; t.s[2 * i] = v.y; t.w[2 * i + 1] = v.z; t.s[2 * i + 1] = v.w;
   }
 }
@@ -463,8 +451,8 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 if (v == 1 && !two) break;
                 const u32* Kb = v ? Kb1 : Kb0;
                 const u32* Ka = Kb + N;
-                const uint4 kb0 = ldg_stream((const uint4*)Kb), kb1 = ldg_stream((const uint4*)Kb + 1);
-                const uint4 ka0 = ldg_stream((const uint4*)Ka), ka1 = ldg_stream((const uint4*)Ka + 1);
+                const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
+                const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
                 const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
                 const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
 #pragma unroll
@@ -605,8 +593,8 @@ k_blind_rotate_cl(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __
             if (v == 1 && !two) break;
             const u32* Kb = v ? Kb1 : Kb0;
             const u32* Ka = Kb + N;
-            const uint4 kb0 = ldg_stream((const uint4*)Kb), kb1 = ldg_stream((const uint4*)Kb + 1);
-            const uint4 ka0 = ldg_stream((const uint4*)Ka), ka1 = ldg_stream((const uint4*)Ka + 1);
+            const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
+            const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
             const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
             const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
 #pragma unroll
