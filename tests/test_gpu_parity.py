@@ -584,6 +584,30 @@ def test_permute_invalid_entries_are_fixed_points():
     assert np.array_equal(got[0], orc.permute(pk, ct[0], ref_perm))
 
 
+@pytest.mark.parametrize("name", ["tiny", "fhew"])
+def test_bootstrap_cuda_graph_capture_and_replay(name):
+    """The bootstrap path is stream-ordered with no host synchronisation, so it can be captured
+    into a CUDA graph once and replayed: replays on new inputs equal direct calls (FHEW-like at
+    B = 7 runs its blind rotations on the cluster kernel and its key switches as cuBLASLt GEMMs)."""
+    cfg, orc, K, ctx, dk = setup(name)
+    rot = ctx.setup_lut(synth.lut(cfg, seed=81))
+    a = T(orc.lwe_encrypt(82, K["s"], synth.messages(cfg, 7, seed=83)))
+    b = T(orc.lwe_encrypt(84, K["s"], synth.messages(cfg, 7, seed=85)))
+    ws = ctx.workspace_bootstrap(7)
+    static_in = a.clone()
+    out = torch.empty_like(a)
+    ctx.bootstrap_batch(dk, rot, static_in, out, ws)              # warm-up outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.bootstrap_batch(dk, rot, static_in, out, ws)
+    for x in (a, b):
+        static_in.copy_(x)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ctx.bootstrap_batch(dk, rot, x))
+
+
 def test_bootstrap_host_buffers_api():
     """fdfb_bootstrap_batch_host (pinned host in/out, copies on the stream) == the device call."""
     cfg, orc, K, ctx, dk = setup("tiny")
