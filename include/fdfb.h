@@ -57,8 +57,11 @@ enum {
 typedef struct fdfb_params {
   uint32_t N;          /* ring degree, power of two in [256, 2048]                         */
   uint32_t n;          /* LWE dimension, 1..4096                                           */
-  uint64_t Q;          /* RLWE prime, Q = 1 mod 2N, Q < 2^55  (the paper: 2^54) */
-  uint32_t log_q_lwe;  /* LWE modulus q_lwe = 2^log_q_lwe, 8..62 (reading c.3)   */
+  uint64_t Q;          /* RLWE prime, Q = 1 mod 2N, Q < 2^55 (Q prime "to compute NTTs",
+                          PAPER.md:2759; the paper's FDFB sets use 62/63-bit Q, PAPER.md:2618;
+                          BASELINE's Large set: 54 bits)                                    */
+  uint32_t log_q_lwe;  /* LWE modulus q_lwe = 2^log_q_lwe, max(8, log2(2N)+1)..55
+                          (reading c.3)                                           */
   uint32_t lwe_key;    /* 0: binary s, u = [1];  1: ternary s, u = [-1, 1] */
   uint32_t rlwe_key;   /* 0: binary, 1: ternary ring secret                                */
   uint32_t logL_rgsw, ell_rgsw;   /* brK gadget   (L = 2^logL, ell = ceil(log_L Q))       */
@@ -67,7 +70,8 @@ typedef struct fdfb_params {
   uint32_t logL_ks, ell_ks;       /* LWE->LWE key ksK mod q_lwe            */
   uint32_t logL_pack, ell_pack;   /* Shift packing key               */
   uint32_t t;          /* plaintext modulus of bootstrap inputs, t | 2N                    */
-  uint32_t sigma_milli;/* Gaussian sigma * 1000 (3200), 0 = noiseless keys (tests)         */
+  uint32_t sigma_milli;/* Gaussian sigma * 1000: 3200 (CDT shipped as data,
+                          reading G17) or 0 = noiseless keys (tests); others UNSUPPORTED    */
 } fdfb_params;
 
 typedef struct fdfb_ctx fdfb_ctx;
@@ -203,7 +207,8 @@ int fdfb_sample_extract(const fdfb_ctx* ctx, const uint64_t* rlwe, const uint32_
 /* LWE KeySwitch N -> n mod q_lwe: in [dev, B x (N+1)] mod q_lwe,
  * out [dev, B x (n+1)].  With workspace [dev] of fdfb_workspace_keyswitch(ctx, B) bytes the
  * switch runs as one exact int8 tensor-core GEMM (digit limbs x balanced base-256 key
- * digits); with workspace NULL through the tiled CUDA-core kernel.  Same bytes. */
+ * digits on the tcgen05 kernel, recombined in its epilogue); with workspace NULL
+ * through the tiled CUDA-core kernel.  Same bytes. */
 size_t fdfb_workspace_keyswitch(const fdfb_ctx* ctx, uint32_t B);
 int fdfb_lwe_keyswitch(const fdfb_ctx* ctx, const void* ksk, const uint64_t* lwe_N, uint64_t* lwe_n,
                        uint32_t B, void* workspace, void* stream);
@@ -245,6 +250,13 @@ int fdfb_shift_streaming(const fdfb_ctx* ctx, const void* pack, const uint64_t* 
  * a, b, c [dev, count x N]. */
 int fdfb_poly_mul(const fdfb_ctx* ctx, const uint64_t* a, const uint64_t* b, uint64_t* c, uint32_t count,
                   void* stream);
+/* The int8 tensor-core contraction under both key switches, Shift and Permute
+ * (kernels_imma.cuh: TMA loads, tcgen05.mma kind::i8, int32 accumulators in TMEM), with its
+ * raw epilogue: D [dev, M x Ncols] int32 = A [dev, M x K] int8 (K-major) x B [dev, Ncols x K]
+ * int8 (K-major)^T, exact.  K must be a positive multiple of 16 and the operands 16-byte
+ * aligned (FDFB_E_DIMENSION / FDFB_E_CUDA otherwise).  Unit test of the GEMM itself. */
+int fdfb_gemm_i8(const fdfb_ctx* ctx, const int8_t* A, const int8_t* B, uint32_t M, uint32_t Ncols, uint32_t K,
+                 int32_t* D, void* stream);
 /* The library's own CDT thresholds (2T values) into thr [host]; *T = tail cut. */
 int fdfb_cdt_table(const fdfb_ctx* ctx, uint64_t* thr, int* T);
 /* Per-kernel-class timing for the roofline report: when enabled, every launch of the

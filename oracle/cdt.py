@@ -3,8 +3,9 @@
 sigma = 3.2, support [-T, T] with T = floor(6 sigma) = 19
 (reading G17 in DESIGN.md).  Thresholds thr[k] = floor(2^64 * CDF(-T + k)) for
 k = 0 .. 2T-1, computed with Python's decimal module at 60 significant digits.
-The CUDA library computes its own table independently (long double); the two
-are compared by tests/test_keygen_parity.py.
+The CUDA library ships its own table as data, generated independently by
+tools/gen_cdt_table.py (binary fixed point); the two are compared for equality by
+tests/test_gpu_parity.py::test_keygen_matches_oracle.
 """
 from decimal import Decimal, getcontext
 

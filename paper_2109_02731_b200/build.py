@@ -10,7 +10,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v",
-         "-L" + CUDA_LIB, "-lcublasLt", "-Xlinker", "-rpath=" + CUDA_LIB]
+         "-L" + CUDA_LIB, "-Xlinker", "-rpath=" + CUDA_LIB]
 
 
 def sources():

@@ -11,7 +11,7 @@
 #include <string>
 #include <vector>
 
-#include <cublasLt.h>
+#include <cudaTypedefs.h>
 
 #include "../../include/fdfb.h"
 #include "kernels_boot.cuh"
@@ -36,8 +36,6 @@ struct fdfb_ctx {
   mutable std::mutex tmu;
   mutable bool timing = false;
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
-  mutable std::mutex lt_mu;
-  mutable cublasLtHandle_t lt = nullptr;   // Shift-as-GEMM (int8 tensor-core GEMM, created lazily)
   int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 batched only, 1 auto (default), 2 / 3 force clusters of NP / 2 NP
 };
 
@@ -110,32 +108,18 @@ static int ceil_log2(u64 x) { int b = 0; while ((1ULL << b) < x) b++; return b; 
 static u64 shoup_of(u64 w, u64 Q) { return (u64)(((u128)w << 64) / Q); }
 static int bitrev(int x, int logn) { int r = 0; for (int i = 0; i < logn; i++) r |= ((x >> i) & 1) << (logn - 1 - i); return r; }
 
-// Library-side CDT for sigma = sigma_milli/1000, support [-T, T], T = floor(6 sigma):
-// thr[k] = floor(2^64 CDF(-T + k)), computed in long double.
-static std::vector<u64> make_cdt(uint32_t sigma_milli, int* Tout) {
-  std::vector<u64> thr;
-  if (sigma_milli == 0) { *Tout = 0; return thr; }
-  long double sg = sigma_milli / 1000.0L;
-  int T = (int)floorl(6 * sg);
-  std::vector<long double> rho;
-  long double Z = 0;
-  for (int e = -T; e <= T; e++) { long double r = expl(-(long double)e * e / (2 * sg * sg)); rho.push_back(r); Z += r; }
-  // lower half from prefix sums, upper half as 2^64 - ceil(2^64 * tail) from tail sums,
-  // so every threshold is computed from a small quantity at full relative precision
-  thr.assign(2 * T, 0);
-  long double acc = 0;
-  for (int k = 0; k < T; k++) {
-    acc += rho[k];
-    thr[k] = (u64)floorl(ldexpl(acc / Z, 64));
-  }
-  long double tail = 0;
-  for (int k = 2 * T - 1; k >= T; k--) {
-    tail += rho[k + 1];                        // sum_{e > -T+k} rho(e)
-    long double v = ceill(ldexpl(tail / Z, 64));
-    thr[k] = (u64)0 - (u64)v;
-  }
-  *Tout = T;
-  return thr;
+// Library-side CDT (reading G17): the thresholds floor(2^64 CDF(-T + k)) for sigma = 3.2 are
+// data, generated once with exact fixed-point arithmetic by tools/gen_cdt_table.py (independent
+// of the oracle's table code); sigma_milli = 0 means noiseless keys, other sigmas are rejected.
+#include "cdt_table.inc"
+static bool make_cdt(uint32_t sigma_milli, std::vector<u64>* thr, int* Tout) {
+  thr->clear();
+  *Tout = 0;
+  if (sigma_milli == 0) return true;
+  if (sigma_milli != kCdtSigmaMilli) return false;
+  thr->assign(kCdtThr, kCdtThr + 2 * kCdtT);
+  *Tout = kCdtT;
+  return true;
 }
 
 // ------------------------------------------------------------------ launch helpers
@@ -301,101 +285,107 @@ static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, in
   return FDFB_E_DIMENSION;
 }
 
-// ------------------------------------------------------------------ exact int8 GEMMs (cuBLASLt)
-// D (row-major [M][Nout] int32) = A (row-major [M][K] int8) x GK^T (GK row-major [Nout][K] int8):
-// column-major "TN" GEMM  D^T (Nout x M) = GK_cm(K x Nout)^T x A_cm(K x M).  K, Nout multiples of 16.
-static const size_t kLtWorkspace = 64ull << 20;
-static int lt_gemm_i8(const fdfb_ctx* c, const int8_t* GK, const int8_t* A, int* D, int M, int K, int Nout,
-                      void* lt_ws, int kclass, cudaStream_t st) {
-  std::lock_guard<std::mutex> lock(c->lt_mu);
-  if (!c->lt) {
-    if (cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) { g_last_cuda = "cublasLtCreate failed"; return FDFB_E_CUDA; }
-  }
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-  cublasLtMatmulPreference_t pref = nullptr;
-  int rc = FDFB_OK;
-  const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-  cublasLtMatmulHeuristicResult_t heur;
-  int nres = 0;
-  const int32_t one = 1, zero = 0;
-  size_t wsb = kLtWorkspace;
-  if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, K, Nout, K) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, K, M, K) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, Nout, M, Nout) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb)) !=
-          CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulAlgoGetHeuristic(c->lt, op, la, lb, lc, lc, pref, 1, &heur, &nres) != CUBLAS_STATUS_SUCCESS ||
-      nres < 1) {
-    g_last_cuda = "cuBLASLt: no int8 TN algorithm";
-    rc = FDFB_E_CUDA;
-  } else {
-    TimedLaunch tl(c, kclass, st);
-    cublasStatus_t s = cublasLtMatmul(c->lt, op, &one, GK, la, A, lb, &zero, D, lc, D, lc, &heur.algo, lt_ws, wsb, st);
-    if (s != CUBLAS_STATUS_SUCCESS) {
-      g_last_cuda = "cublasLtMatmul failed: " + std::to_string((int)s);
-      rc = FDFB_E_CUDA;
-    }
-    c->launches++;
-  }
-  if (pref) cublasLtMatmulPreferenceDestroy(pref);
-  if (lc) cublasLtMatrixLayoutDestroy(lc);
-  if (lb) cublasLtMatrixLayoutDestroy(lb);
-  if (la) cublasLtMatrixLayoutDestroy(la);
-  if (op) cublasLtMatmulDescDestroy(op);
-  return rc;
+// ------------------------------------------------------------------ exact int8 GEMMs (kernels_imma.cuh)
+// TMA descriptors come from the driver's cuTensorMapEncodeTiled, resolved through the runtime
+// (no libcuda link); one 2D map per K-major int8 operand [rows][K] with row pitch ld bytes.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+    cudaGetLastError();
+  });
+  return fn;
+}
+static int make_tmap_i8(CUtensorMap* m, const void* base, size_t rows, size_t K, size_t ld, int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) { g_last_cuda = "cuTensorMapEncodeTiled unavailable"; return FDFB_E_CUDA; }
+  if (((uintptr_t)base & 15) || (ld & 15) || K > ld) { g_last_cuda = "GEMM operand not 16-byte aligned"; return FDFB_E_CUDA; }
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)imma::BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { g_last_cuda = "cuTensorMapEncodeTiled failed: " + std::to_string((int)r); return FDFB_E_CUDA; }
+  return FDFB_OK;
+}
+// D = A [M][K] (pitch lda) x B [Ncols][K]^T (pitch ldb), both int8 K-major, through the
+// epilogue e (kernels_imma.cuh); Ncols is a multiple of imma::BN except in raw mode.
+static int imma_gemm(const fdfb_ctx* c, const int8_t* A, size_t M, size_t lda, const int8_t* B, size_t Ncols,
+                     size_t ldb, size_t K, const ImmaEpi& e, int kclass, cudaStream_t st) {
+  if (M == 0) return FDFB_OK;
+  CUtensorMap ta, tb;
+  int rc = make_tmap_i8(&ta, A, M, K, lda, imma::BM);
+  if (!rc) rc = make_tmap_i8(&tb, B, Ncols, K, ldb, imma::BN);
+  if (rc) return rc;
+  const int tiles_m = (int)((M + imma::BM - 1) / imma::BM), tiles_n = (int)((Ncols + imma::BN - 1) / imma::BN);
+  const long long nt = (long long)tiles_m * tiles_n;
+  const int grid = (int)(nt < c->num_sms ? nt : c->num_sms);
+  CK(cudaFuncSetAttribute(k_imma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)imma::SMEM));
+  TimedLaunch tl(c, kclass, st);
+  k_imma<<<grid, imma::THREADS, imma::SMEM, st>>>(ta, tb, (int)K, tiles_m, tiles_n, c->dp, e);
+  CKL(c);
+  return FDFB_OK;
 }
 
 // ------------------------------------------------------------------ key switching
 static KsGemm ks_shape_rlwe(const fdfb_params& p) { return ks_gemm_shape(p.N, p.ell_pk, p.logL_pk, 2 * p.N); }
 static KsGemm ks_shape_lwe(const fdfb_params& p) { return ks_gemm_shape(p.N, p.ell_ks, p.logL_ks, p.n + 1); }
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-static const size_t kKsDBytes = 1ull << 30;     // int32 product chunk cap
+static const size_t kKsABytes = 1ull << 30;     // int8 limb-matrix chunk cap
 static int ks_chunk_rows(const KsGemm& g) {     // LWE samples per GEMM chunk
-  size_t r = kKsDBytes / ((size_t)g.NL * g.Nout * 4);
+  size_t r = kKsABytes / ((size_t)g.NLP * g.Kd);
   return (int)(r < 1 ? 1 : (r > (1 << 20) ? (1 << 20) : r));
 }
 static size_t ks_ws_bytes(const KsGemm& g, int count) {
   const int rows = count < ks_chunk_rows(g) ? count : ks_chunk_rows(g);
-  return align256((size_t)rows * g.NL * g.Kd) + align256((size_t)rows * g.NL * g.Nout * 4) + kLtWorkspace;
+  return align256((size_t)rows * g.NLP * g.Kd);
 }
 // device formats: canonical key, then (256-aligned) its int8 digit matrix
 static size_t ks_key_bytes(size_t canon, const KsGemm& g) { return align256(canon) + (size_t)g.Nout * g.Kd; }
-static int ks_build_key(const fdfb_ctx* c, const u64* canon_dev, size_t canon_bytes, const KsGemm& g, void* dev,
-                        cudaStream_t st) {
+// qbits = 0: key mod Q; else key mod 2^qbits (digits of the centred representative)
+static int ks_build_key(const fdfb_ctx* c, const u64* canon_dev, size_t canon_bytes, const KsGemm& g, int qbits,
+                        void* dev, cudaStream_t st) {
   if ((void*)canon_dev != dev) CK(cudaMemcpyAsync(dev, canon_dev, canon_bytes, cudaMemcpyDeviceToDevice, st));
   int8_t* GK = (int8_t*)dev + align256(canon_bytes);
   dim3 grd((g.Kd + 31) / 32, (g.Wpad + 7) / 8), blk(32, 8);
-  k_ks_gemm_key<<<grd, blk, 0, st>>>((const u64*)dev, g, GK);
+  k_ks_gemm_key<<<grd, blk, 0, st>>>((const u64*)dev, g, c->prm.Q, qbits, GK);
   CKL(c);
   return FDFB_OK;
 }
-// out = KeySwitch(lwe) for `count` samples through the GEMM, chunked; qmask = 0 -> mod Q.
+// out = KeySwitch(lwe) for `count` samples: limb matrix, then one tcgen05 GEMM per chunk with
+// the recombination and b - v in its epilogue; qmask = 0 -> mod Q, else mod 2^w.
 static int ks_gemm(const fdfb_ctx* c, const void* key_dev, size_t canon_bytes, const KsGemm& g, int logL, int ell,
                    const u64* lwe, int count, u64* out, u64 qmask, void* ws, int kclass, cudaStream_t st) {
   const int N = c->prm.N;
   const int8_t* GK = (const int8_t*)key_dev + align256(canon_bytes);
   const int CH = ks_chunk_rows(g);
-  const int rows0 = count < CH ? count : CH;
   int8_t* A = (int8_t*)ws;
-  int* D = (int*)((char*)ws + align256((size_t)rows0 * g.NL * g.Kd));
-  void* lt_ws = (char*)D + align256((size_t)rows0 * g.NL * g.Nout * 4);
   for (int o = 0; o < count; o += CH) {
     const int rows = (count - o) < CH ? (count - o) : CH;
     const u64* in = lwe + (size_t)o * (N + 1);
     dim3 gb((g.Kd + 255) / 256 < 64 ? (g.Kd + 255) / 256 : 64, rows);
     k_ks_gemm_bits<<<gb, 256, 0, st>>>(in, rows, N, ell, logL, g, A);
     CKL(c);
-    int rc = lt_gemm_i8(c, GK, A, D, rows * g.NL, g.Kd, g.Nout, lt_ws, kclass, st);
+    ImmaEpi e;
+    e.mode = qmask ? 1 : 0;
+    e.nlp = g.NLP;
+    e.rows = rows * g.NLP;
+    e.W = g.W;
+    e.ldo = g.W;
+    e.neg_sub = 1;
+    e.qmask = qmask;
+    e.out = out + (size_t)o * g.W;
+    e.lwe = in;
+    e.lwe_ld = N + 1;
+    int rc = imma_gemm(c, A, (size_t)rows * g.NLP, g.Kd, GK, g.Nout, g.Kd, g.Kd, e, kclass, st);
     if (rc) return rc;
-    const size_t tot = (size_t)rows * g.W;
-    k_ks_gemm_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, D, in, rows, N, g, c->prm.Q, qmask,
-                                                                     out + (size_t)o * g.W);
-    CKL(c);
   }
   return FDFB_OK;
 }
@@ -410,7 +400,9 @@ static int validate(const fdfb_params* p) {
   if (!(p->N == 256 || p->N == 512 || p->N == 1024 || p->N == 2048)) return FDFB_E_DIMENSION;
   if (p->n < 1 || p->n > 4096) return FDFB_E_DIMENSION;
   if (p->Q < 3 || p->Q >= (1ULL << 55) || !h_is_prime(p->Q) || (p->Q - 1) % (2 * (u64)p->N)) return FDFB_E_NON_NTT_MODULUS;
-  if (p->log_q_lwe < 8 || p->log_q_lwe > 62 || p->log_q_lwe < (uint32_t)ceil_log2(2 * p->N) + 1) return FDFB_E_DIMENSION;
+  // q_lwe <= 2^55: the key switches' int8 GEMM splits the centred key (|v| <= 2^54) into 7
+  // balanced base-256 digits
+  if (p->log_q_lwe < 8 || p->log_q_lwe > 55 || p->log_q_lwe < (uint32_t)ceil_log2(2 * p->N) + 1) return FDFB_E_DIMENSION;
   if (p->lwe_key > 1 || p->rlwe_key > 1) return FDFB_E_UNSUPPORTED;
   const int qb = bits_of(p->Q - 1) > 0 ? ceil_log2(p->Q) : 1;
   auto ok = [](uint32_t logL, uint32_t ell, int bits) {
@@ -422,6 +414,9 @@ static int validate(const fdfb_params* p) {
   if (!ok(p->logL_ks, p->ell_ks, (int)p->log_q_lwe)) return FDFB_E_DECOMP;
   if (!ok(p->logL_pack, p->ell_pack, qb) || p->logL_pack > 12) return FDFB_E_DECOMP;
   if ((u128)p->N * p->ell_pk * (1ULL << p->logL_pk) >= ((u128)1 << 32)) return FDFB_E_DECOMP;
+  // key-switch GEMM sums stay exact in int32: K = N ell terms of |limb x digit| <= 127 * 128
+  if ((u64)p->N * p->ell_pk * 127 * 128 >= (1ULL << 31) || (u64)p->N * p->ell_ks * 127 * 128 >= (1ULL << 31))
+    return FDFB_E_DECOMP;
   if (p->t < 2 || (2 * p->N) % p->t) return FDFB_E_PLAINTEXT;
   return FDFB_OK;
 }
@@ -565,7 +560,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   if (!psi) { delete c; return FDFB_E_NON_NTT_MODULUS; }
   u64 psi_inv = h_powmod(psi, Q - 2, Q);
   int T = 0;
-  c->cdt = make_cdt(p->sigma_milli, &T);
+  if (!make_cdt(p->sigma_milli, &c->cdt, &T)) { delete c; return FDFB_E_UNSUPPORTED; }
   // tables: tw, twp, itw, itwp (N each), cdt (2T), omega (N)
   size_t ntab = 4 * (size_t)N + c->cdt.size() + N;
   std::vector<u64> h(ntab, 0);
@@ -627,7 +622,6 @@ extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
   cudaFree(c->d_rtab);
-  if (c->lt) cublasLtDestroy(c->lt);
   delete c;
   cudaSetDevice(cur);
 }
@@ -775,13 +769,13 @@ extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int
       int cnt = (int)((ent - o) < (size_t)CH ? (ent - o) : CH);
       rc = rlwe_entries(c, seed, 2, sk_lwe, sk_rlwe, nullptr, o, cnt, (u64*)bpk + o * 2 * N, shat, tmask, tprod, st);
     }
-    if (!rc) rc = ks_build_key(c, (const u64*)bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), bpk, st);
+    if (!rc) rc = ks_build_key(c, (const u64*)bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), 0, bpk, st);
   }
   if (!rc && (which & 8)) {
     int ent = N * p.ell_ks;
     k_ksk_gen<<<(ent * 32 + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe, nullptr, 0, ent, (u64*)ksk);
     CKL(c);
-    rc = ks_build_key(c, (const u64*)ksk, canon_ksk_bytes(p), ks_shape_lwe(p), ksk, st);
+    rc = ks_build_key(c, (const u64*)ksk, canon_ksk_bytes(p), ks_shape_lwe(p), (int)p.log_q_lwe, ksk, st);
   }
   if (!rc && (which & 16)) rc = pack_keygen(c, seed, sk_rlwe, pack, shat, tmask, tprod, tout, CH, st);
   cudaFreeAsync(shat, st); cudaFreeAsync(tmask, st); cudaFreeAsync(tprod, st); cudaFreeAsync(tout, st);
@@ -842,9 +836,9 @@ extern "C" int fdfb_key_import(const fdfb_ctx* c, int kind, const uint64_t* cano
     }
     cudaFreeAsync(tmp, st);
   } else if (kind == FDFB_KEY_BPK) {
-    rc = ks_build_key(c, canon, sz.canon_bpk, ks_shape_rlwe(p), dev_key, st);
+    rc = ks_build_key(c, canon, sz.canon_bpk, ks_shape_rlwe(p), 0, dev_key, st);
   } else if (kind == FDFB_KEY_KSK) {
-    rc = ks_build_key(c, canon, sz.canon_ksk, ks_shape_lwe(p), dev_key, st);
+    rc = ks_build_key(c, canon, sz.canon_ksk, ks_shape_lwe(p), (int)p.log_q_lwe, dev_key, st);
   } else if (kind == FDFB_KEY_PACK) {
     rc = pack_import(c, canon, dev_key, st);
   } else {
@@ -947,16 +941,9 @@ extern "C" int fdfb_blind_rotate(const fdfb_ctx* c, const void* brk, uint64_t* a
 
 static int keyswitch_rlwe(const fdfb_ctx* c, const u64* bpk, const u64* lwe, int count, u64* out, void* ws,
                           cudaStream_t st) {
-  if (ws) {
-    const fdfb_params& p = c->prm;
-    return ks_gemm(c, bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), p.logL_pk, p.ell_pk, lwe, count, out, 0, ws,
-                   FDFB_KCLASS_KEYSWITCH_RLWE, st);
-  }
-  dim3 grd((2 * c->prm.N) / KS_COLS, (count + KS_ROWS - 1) / KS_ROWS);
-  TimedLaunch tl(c, FDFB_KCLASS_KEYSWITCH_RLWE, st);
-  k_keyswitch_rlwe<<<grd, KS_COLS, 0, st>>>(c->dp, bpk, lwe, count, out);
-  CKL(c);
-  return FDFB_OK;
+  const fdfb_params& p = c->prm;
+  return ks_gemm(c, bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), p.logL_pk, p.ell_pk, lwe, count, out, 0, ws,
+                 FDFB_KCLASS_KEYSWITCH_RLWE, st);
 }
 static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int count, u64* out, void* ws,
                          cudaStream_t st) {
@@ -1217,11 +1204,24 @@ extern "C" int fdfb_timing_read(const fdfb_ctx* c, int kclass, double* total_ms,
 }
 extern "C" uint64_t fdfb_launch_count(const fdfb_ctx* c) { return c ? (uint64_t)c->launches.load() : 0; }
 
+// Parity hook of the tcgen05 int8 GEMM itself: D [M][Ncols] int32 = A [M][K] x B [Ncols][K]^T.
+extern "C" int fdfb_gemm_i8(const fdfb_ctx* c, const int8_t* A, const int8_t* B, uint32_t M, uint32_t Ncols,
+                            uint32_t K, int32_t* D, void* stream) {
+  if (!c) return FDFB_E_NULL;
+  if (!M || !Ncols) return FDFB_OK;
+  if (!A || !B || !D) return FDFB_E_NULL;
+  if (K == 0 || K % 16) return FDFB_E_DIMENSION;
+  ImmaEpi e;
+  e.mode = 2; e.nlp = 1; e.rows = (int)M; e.W = (int)Ncols; e.ldo = (int)Ncols; e.neg_sub = 0;
+  e.qmask = 0; e.out = D; e.lwe = nullptr; e.lwe_ld = 0;
+  return imma_gemm(c, A, M, K, B, Ncols, K, K, e, FDFB_KCLASS_SHIFT_GEMM, S(stream));
+}
+
 extern "C" const char* fdfb_status_string(int s) {
   switch (s) {
     case FDFB_OK: return "ok";
     case FDFB_E_NULL: return "null pointer argument";
-    case FDFB_E_NON_NTT_MODULUS: return "Q is not a prime with Q = 1 mod 2N (or Q >= 2^56)";
+    case FDFB_E_NON_NTT_MODULUS: return "Q is not a prime with Q = 1 mod 2N (or Q >= 2^55)";
     case FDFB_E_DIMENSION: return "dimension out of range";
     case FDFB_E_DECOMP: return "gadget decomposition: ell != ceil(bits / logL) or out of range";
     case FDFB_E_INDEX: return "index out of range";

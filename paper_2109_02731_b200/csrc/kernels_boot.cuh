@@ -80,59 +80,12 @@ __global__ void k_extract_modswitch(DevParams p, const u64* __restrict__ accs, i
 }
 
 // ---------------------------------------------------------------------------
-// a5 (KeySwitch LWE_N -> RLWE with bpK), batched as a
-// digit-matrix x key-matrix product:  out[g] = [b_g, 0] - sum_{i,j} Decomp(a_{g,i})[j] * bpK[i,j].
-// CTA tile: KS_ROWS ciphertexts x KS_COLS output coefficients (of 2N).  Exact
-// accumulation: key split in 32-bit halves, digit (< 2^logL) x half accumulated
-// in u64 (no overflow for N*ell*2^logL*2^32 < 2^64), reduced mod Q at the end.
+// a6 CUDA-core LWE KeySwitch N -> n mod q_lwe, the tiled reference
+// evaluation behind fdfb_lwe_keyswitch with a NULL workspace (the bootstrap uses the tcgen05
+// GEMM of kernels_ksgemm.cuh).  CTA tile: KS_ROWS ciphertexts x KS_COLS output words;
+// arithmetic mod 2^w is native u64 wrap.
 #define KS_ROWS 16
 #define KS_COLS 128
-__global__ void __launch_bounds__(KS_COLS)
-k_keyswitch_rlwe(DevParams p, const u64* __restrict__ bpk, const u64* __restrict__ lwe, int count,
-                 u64* __restrict__ out) {
-  const int N = p.N, ell = p.ell_pk, logL = p.logL_pk;
-  const u64 Q = p.Q, dmask = (1ULL << logL) - 1;
-  const int col = blockIdx.x * KS_COLS + threadIdx.x;   // in [0, 2N)
-  const int row0 = blockIdx.y * KS_ROWS;
-  __shared__ u64 sa[KS_ROWS][33];
-  u64 lo[KS_ROWS], hi[KS_ROWS];
-#pragma unroll
-  for (int r = 0; r < KS_ROWS; r++) { lo[r] = 0; hi[r] = 0; }
-  for (int i0 = 0; i0 < N; i0 += 32) {
-    __syncthreads();
-    for (int x = threadIdx.x; x < KS_ROWS * 32; x += KS_COLS) {
-      int r = x / 32, ii = x % 32;
-      int g = row0 + r;
-      sa[r][ii] = (g < count && i0 + ii < N) ? lwe[(size_t)g * (N + 1) + 1 + i0 + ii] : 0;
-    }
-    __syncthreads();
-    for (int ii = 0; ii < 32 && i0 + ii < N; ii++) {
-      const u64* krow = bpk + ((size_t)(i0 + ii) * ell) * 2 * N + col;
-      for (int j = 0; j < ell; j++) {
-        u64 kv = __ldg(krow + (size_t)j * 2 * N);
-        u32 klo = (u32)kv, khi = (u32)(kv >> 32);
-#pragma unroll
-        for (int r = 0; r < KS_ROWS; r++) {
-          u32 dg = (u32)((sa[r][ii] >> (j * logL)) & dmask);
-          lo[r] += (u64)dg * klo;
-          hi[r] += (u64)dg * khi;
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < KS_ROWS; r++) {
-    int g = row0 + r;
-    if (g >= count) continue;
-    unsigned __int128 s = ((unsigned __int128)hi[r] << 32) + lo[r];
-    u64 v = neg_mod((u64)(s % Q), Q);
-    if (col == 0) v = add_mod(v, lwe[(size_t)g * (N + 1)], Q);
-    out[(size_t)g * 2 * N + col] = v;
-  }
-}
-
-// a6 (second half): LWE KeySwitch N -> n mod q_lwe, same tiling;
-// arithmetic mod 2^w is native u64 wrap.
 __global__ void __launch_bounds__(KS_COLS)
 k_keyswitch_lwe(DevParams p, const u64* __restrict__ ksk, const u64* __restrict__ lwe, int count,
                 u64* __restrict__ out) {

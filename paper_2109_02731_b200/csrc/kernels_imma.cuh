@@ -1,0 +1,277 @@
+// kernels_imma.cuh -- the exact int8 tensor-core contraction behind both key switches
+// (PAPER.md:3006-3013), Shift's VectorPack and Permute
+// (PAPER.md:124-139): a hand-written sm_100a GEMM on the 5th-generation tensor cores.
+//
+//   D[r][c] = sum_k A[r][k] * B[c][k]          (int8 x int8 -> int32, exact)
+//
+// A (rows = digit limbs / 0-1 rows of the ciphertexts) and B (rows = balanced base-256
+// digits of the key coefficients) are both K-major in global memory.  Per CTA (one per
+// SM, persistent over the output tiles, 256 threads, warp-specialised):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2D loads of a 128 x 128 B tile of A and
+//               a BN x 128 B tile of B per stage (SWIZZLE_128B), STAGES-deep mbarrier ring;
+//   warp 1      MMA issuer (one thread): tcgen05.mma.cta_group::1.kind::i8, M = 128,
+//               N = BN, K = 32 per instruction, accumulators (int32) in TMEM, two
+//               accumulator buffers so the epilogue of tile t overlaps the MMAs of t + 1;
+//   warp 2      TMEM allocator (512 columns);
+//   warps 4..7  epilogue: tcgen05.ld of the accumulator rows (one TMEM lane = one row per
+//               thread) and the exact recombination of the digit planes, see below.
+//
+// Column layout of B (built by the key-digit kernels): an output tile of BN = 7 WT
+// columns holds the 7 digit planes of WT consecutive output words,
+//   column (nb, l, wi) = nb * 7 WT + l * WT + wi,   word w = nb * WT + wi,
+// so the epilogue has every digit of a word in one tile and writes the recombined word:
+//   v = sum_{l<7} 256^l D_l   (mod Q by Horner/Barrett, or mod 2^64 by wrapping),
+//   limb rows: NLP consecutive rows r = g NLP + t of A hold 7-bit limbs t of the same
+//   digits, combined across lanes: v_g = sum_t 128^t v_{g,t};
+//   out[g][w] = b_g [w = 0] - v_g  (key switch: mod Q or & qmask)  or  out[g][w] = v_g.
+// A raw mode writes the int32 accumulators (parity test of the GEMM itself).
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+
+namespace imma {
+constexpr int BM = 128;                      // rows per tile (TMEM lanes)
+constexpr int BK = 128;                      // K bytes per stage (one 128-byte swizzle atom)
+constexpr int WT = 32;                       // output words per tile
+constexpr int BN = 7 * WT;                   // 224 accumulator columns per tile
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;             // 16 KB
+constexpr int B_BYTES = BN * BK;             // 28 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int ACC_COLS = 256;                // TMEM columns per accumulator buffer (2 buffers)
+constexpr int THREADS = 256;
+constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+}  // namespace imma
+
+// epilogue parameters
+struct ImmaEpi {
+  int mode;            // 0: mod Q, 1: mod 2^64 then & qmask, 2: raw int32
+  int nlp;             // limb rows per output row (1, 2 or 4); raw: 1
+  int rows;            // valid rows of A (M)
+  int W;               // valid output words per row (raw: valid columns)
+  int ldo;             // output row stride (u64 words; raw: int32 words)
+  int neg_sub;         // 1: out = b - v (key switch), 0: out = v
+  u64 qmask;
+  void* out;
+  const u64* lwe;      // b_g = lwe[g * lwe_ld] (neg_sub), may be null
+  long long lwe_ld;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+FDFB_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+FDFB_DEV void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+FDFB_DEV void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+FDFB_DEV void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+FDFB_DEV void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+FDFB_DEV void tma_load_2d(const CUtensorMap* tm, void* dst, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+FDFB_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+FDFB_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// K-major, 128-byte-swizzled operand tile: rows of 128 B, 8-row groups 1024 B apart
+FDFB_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)1 << 16;                          // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: kind::i8, D = s32, A = B = signed int8, both K-major, M x N
+__host__ __device__ constexpr uint32_t umma_idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+FDFB_DEV void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+FDFB_DEV void umma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+// 32 lanes x 32 bits, 8 consecutive columns per thread
+FDFB_DEV void tmem_ld8(uint32_t taddr, int (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+FDFB_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(imma::THREADS, 1)
+k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int tiles_m,
+       int tiles_n, DevParams dp, ImmaEpi e) {
+  using namespace imma;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // SW128 atoms: 1024-B aligned
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = (uint32_t*)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = tiles_m * tiles_n;
+  const int nk = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int b = 0; b < 2; b++) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {                                   // ---- TMA producer
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        for (int kb = 0; kb < nk; kb++) {
+          mbar_wait(empty + st, ph ^ 1);
+          uint8_t* sa = smem + st * STAGE_BYTES;
+          mbar_expect_tx(full + st, STAGE_BYTES);
+          tma_load_2d(&tmA, sa, full + st, kb * BK, tm * BM);
+          tma_load_2d(&tmB, sa + A_BYTES, full + st, kb * BK, tn * BN);
+          if (++st == STAGES) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                   // ---- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_i8(BM, BN);
+      int st = 0, ab = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(tempty + ab, aph ^ 1);              // epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(ab * ACC_COLS);
+        for (int kb = 0; kb < nk; kb++) {
+          mbar_wait(full + st, ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 32; k++)
+            umma_i8(d, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), idesc, (kb | k) != 0);
+          umma_commit(empty + st);                     // smem slot free once these MMAs retire
+          if (++st == STAGES) { st = 0; ph ^= 1; }
+        }
+        umma_commit(tfull + ab);                       // accumulator complete
+        if (++ab == 2) { ab = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {                              // ---- epilogue (lane quarter = warp % 4)
+    const int q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      mbar_wait(tfull + ab, aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * ACC_COLS);
+      const int row = tm * BM + row_in_tile;
+      if (e.mode == 2) {                               // raw int32 accumulators
+        int* o = (int*)e.out + (size_t)row * e.ldo;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 8) {
+          int v[8];
+          tmem_ld8(tbase + c, v);
+          tmem_ld_wait();
+          const int col = tn * BN + c;
+          if (row < e.rows) {
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+              if (col + i < e.W) o[col + i] = v[i];
+          }
+        }
+      } else {
+        const int nlp = e.nlp;
+        const int g = row / nlp, t = row % nlp;       // output row, limb
+        const int lbase = lane & ~(nlp - 1);
+        u64* o = (u64*)e.out + (size_t)g * e.ldo;
+        const bool wrap = e.mode == 1;
+#pragma unroll 1
+        for (int c8 = 0; c8 < WT; c8 += 8) {
+          int v[7][8];
+#pragma unroll
+          for (int l = 0; l < 7; l++) tmem_ld8(tbase + l * WT + c8, v[l]);
+          tmem_ld_wait();
+          u64 val[8];
+#pragma unroll
+          for (int i = 0; i < 8; i++) {
+            u64 s = 0;
+            if (wrap) {
+#pragma unroll
+              for (int l = 6; l >= 0; l--) s = (s << 8) + (u64)(long long)v[l][i];
+            } else {
+#pragma unroll
+              for (int l = 6; l >= 0; l--) s = horner_mod(s, 8, v[l][i], dp);
+            }
+            // limbs t of output row g sit in lanes lbase .. lbase + nlp - 1: sum_t 128^t s_t
+            u64 acc = 0;
+            for (int tt = nlp - 1; tt >= 0; tt--) {
+              const u64 st = __shfl_sync(0xffffffffu, s, lbase + tt);
+              acc = wrap ? (acc << 7) + st : add_mod(horner_mod(acc, 7, 0, dp), st, dp.Q);
+            }
+            val[i] = acc;
+          }
+          const int w0 = tn * WT + c8;
+          if (row < e.rows) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+              const int w = w0 + i;
+              if ((i % nlp) != t || w >= e.W) continue;  // the nlp lanes of a row split the words
+              u64 r = val[i];
+              if (e.neg_sub) {
+                const u64 b = (w == 0 && e.lwe) ? __ldg(e.lwe + (size_t)g * e.lwe_ld) : 0;
+                r = wrap ? ((b - r) & e.qmask) : sub_mod(b, r, dp.Q);
+              } else if (wrap) {
+                r &= e.qmask;
+              }
+              o[w] = r;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty + ab);
+      if (++ab == 2) { ab = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}

@@ -23,6 +23,7 @@
 // the definition's m * N * ell; the result is the same residue vector mod Q.
 #pragma once
 #include "kernels_core.cuh"
+#include "kernels_ksgemm.cuh"
 
 struct PackLayout {
   size_t P;                 // words per RLWE (2N)
@@ -342,7 +343,8 @@ k_vector_pack(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64
 // the GK = ell(N-1) + N + ell N "terms") times the key matrix whose row for each term is
 // the term polynomial pair.  Key coefficients (< 2^54) are split into 7 balanced base-256
 // digits, so the product is 7 int8 GEMMs done as one (N_out = 7 * 2N), exact in int32
-// (|sum| <= GK * 128 < 2^31); k_shift_gemm_finish recombines the digits mod Q.
+// (|sum| <= GK * 128 < 2^31), on the tcgen05 kernel (kernels_imma.cuh) whose epilogue
+// recombines the digits mod Q; k_shift_gemm_finish assembles the output.
 struct ShiftGemm {
   int K;        // number of terms ell(N-1) + N + ell N
   int Kpad;     // K rounded up to a multiple of 16
@@ -391,7 +393,8 @@ __global__ void k_shift_s0(DevParams p, const u64* __restrict__ pk, PackLayout l
   for (int j = 0; j < p.ell_pack; j++) s = add_mod(s, pk[lay.T1 + ((size_t)j * 2) * lay.P + w], p.Q);
   S0[w] = s;
 }
-// GK[l * 2N + w][kk] = balanced digit l of term kk at coefficient w.  Tile: 32 terms x 8 coefficients.
+// GK[imma_key_row(l, w)][kk] = balanced digit l of term kk (centred mod Q) at coefficient w.
+// Tile: 32 terms x 8 coefficients.
 __global__ void k_shift_gemm_key(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ S0,
                                  ShiftGemm g, int8_t* __restrict__ GK) {
   const int kk = blockIdx.x * 32 + threadIdx.x;
@@ -400,13 +403,10 @@ __global__ void k_shift_gemm_key(DevParams p, const u64* __restrict__ pk, PackLa
   u64 v = 0;
   if (kk < g.K) v = shift_term(p, pk, lay, S0, kk, w);
   if (kk >= g.Kpad) return;
+  int8_t dg[7];
+  balanced_digits7(centred(v, p.Q, 0), dg);
 #pragma unroll
-  for (int l = 0; l < 7; l++) {
-    int t = (int)(v & 255);
-    if (t >= 128) t -= 256;
-    v = (u64)((long long)v - t) >> 8;
-    GK[((size_t)l * 2 * p.N + w) * g.Kpad + kk] = (int8_t)t;
-  }
+  for (int l = 0; l < 7; l++) GK[imma_key_row(l, w) * g.Kpad + kk] = dg[l];
 }
 // Per-batch 0/1 matrix: rows 2c (G) and 2c+1 (Bs) of ciphertext c.  Grid (ceil(N / blockDim), B):
 // thread t computes the SampleExt coefficients it needs once and writes their ell bits with
@@ -443,13 +443,13 @@ __global__ void k_shift_bits(DevParams p, const u64* __restrict__ ct, const u32*
   }
   for (int kk = g.K + t; kk < g.Kpad; kk += N) { rg[kk] = 0; rb[kk] = 0; }
 }
-// Recombine digits (int32 D[row][l * 2N + w]) mod Q and assemble Shift's output, one CTA
-// of 256 threads per (ciphertext, column):  S = G + U - X^m (U + Bs);  P = [bsum, 0] - S;
+// Assemble Shift's output from the GEMM's recombined rows (V[row][w] mod Q, rows 2c = G and
+// 2c+1 = Bs), one CTA of 256 threads per (ciphertext, column):  S = G + U - X^m (U + Bs);  P = [bsum, 0] - S;
 // branch 1: out = ct X^d + 2P;  branch 2: out = (2P - ct) X^d.
 template <int CPT>
 __global__ void __launch_bounds__(256)
 k_shift_gemm_finish(DevParams p, const u64* __restrict__ pk, PackLayout lay, const u64* __restrict__ ct,
-                    const u32* __restrict__ dd, const int* __restrict__ D, u64* __restrict__ out) {
+                    const u32* __restrict__ dd, const u64* __restrict__ V, u64* __restrict__ out) {
   constexpr int TPB = 256;
   const int N = p.N, c = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const u64 Q = p.Q;
@@ -463,22 +463,15 @@ k_shift_gemm_finish(DevParams p, const u64* __restrict__ pk, PackLayout lay, con
   }
   const bool br1 = 2 * d <= N;
   const int m = br1 ? d : N - d, K1 = br1 ? N - d + 1 : 1;
-  const int Nout = 7 * 2 * N;
-  const int* dg = D + (size_t)(2 * c) * Nout + (size_t)h * N;
-  const int* db = dg + Nout;
+  const u64* vgr = V + (size_t)(2 * c) * 2 * N + (size_t)h * N;
+  const u64* vbr = vgr + 2 * N;
   const u64* U = pk + lay.U + (size_t)h * N;
   u64 G[CPT];
 #pragma unroll
   for (int r = 0; r < CPT; r++) {
     const int x = tid + r * TPB;
-    u64 vg = 0, vb = 0;                        // sum_l digit_l 256^l mod Q (Horner, Barrett)
-#pragma unroll
-    for (int l = 6; l >= 0; l--) {
-      vg = horner_mod(vg, 8, dg[(size_t)l * 2 * N + x], p);
-      vb = horner_mod(vb, 8, db[(size_t)l * 2 * N + x], p);
-    }
-    G[r] = vg;
-    W[x] = add_mod(__ldg(U + x), vb, Q);
+    G[r] = __ldg(vgr + x);
+    W[x] = add_mod(__ldg(U + x), __ldg(vbr + x), Q);
   }
   __syncthreads();
   const u64* cth = ct + (size_t)c * 2 * N + (size_t)h * N;
@@ -513,27 +506,24 @@ k_shift_gemm_finish(DevParams p, const u64* __restrict__ pk, PackLayout lay, con
 // (A_j = Decomp(SampleExt(ct, j).a); the constant pK[.,.,0] parts cancel for L = 2).
 // L == 2: every moved slot i is one GEMM row with coefficients A_j - A_i in {-1, 0, 1} against
 // the key matrix of Delta0_{k,l} = pK[k,l,1] - pK[k,l,0] (7 balanced base-256 digits, int8),
-// exact in int32 (|sum| <= N ell 128 < 2^31); k_permute_finish recombines, rotates and adds.
+// exact in int32 (|sum| <= N ell 128 < 2^31); the GEMM epilogue recombines the digits mod Q,
+// k_permute_partial / k_permute_reduce rotate and add.
 struct PermGemm { int K; int Nout; };          // K = N ell (multiple of 16), Nout = 7 * 2N
 static inline PermGemm perm_gemm_shape(int N, int ell) { PermGemm g; g.K = N * ell; g.Nout = 14 * N; return g; }
 static inline size_t perm_gemm_key_bytes(int N, int ell, int L) {
   return L == 2 ? (size_t)14 * N * (size_t)N * ell : 0;
 }
-// GP[l * 2N + w][k*ell + j] = digit l of Delta0_{k,j}[w]
+// GP[imma_key_row(l, w)][k*ell + j] = digit l of Delta0_{k,j}[w] (centred mod Q)
 __global__ void k_perm_gemm_key(DevParams p, const u64* __restrict__ pk, PackLayout lay, PermGemm g,
                                 int8_t* __restrict__ GP) {
   const int kk = blockIdx.x * 32 + threadIdx.x;   // (k, j) row of the canonical table
   const int w = blockIdx.y * 8 + threadIdx.y;
   if (kk >= g.K || w >= 2 * p.N) return;
   const u64* e = pk + lay.A + (size_t)kk * 2 * lay.P;                    // pK[k,j,0], then pK[k,j,1]
-  u64 v = sub_mod(e[lay.P + w], e[w], p.Q);
+  int8_t dg[7];
+  balanced_digits7(centred(sub_mod(e[lay.P + w], e[w], p.Q), p.Q, 0), dg);
 #pragma unroll
-  for (int l = 0; l < 7; l++) {
-    int t = (int)(v & 255);
-    if (t >= 128) t -= 256;
-    v = (u64)((long long)v - t) >> 8;
-    GP[((size_t)l * 2 * p.N + w) * g.K + kk] = (int8_t)t;
-  }
+  for (int l = 0; l < 7; l++) GP[imma_key_row(l, w) * g.K + kk] = dg[l];
 }
 // rows r = c_local * N + (i-1) of a chunk of ciphertexts: A[r][k*ell + l] = bit_l(a'_j[k]) - bit_l(a'_i[k]),
 // j = pi(i); zero rows for fixed points (and flag an invalid permutation entry).  One CTA of
@@ -566,7 +556,7 @@ k_perm_bits(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ per
 template <int CPT>
 __global__ void __launch_bounds__(256)
 k_permute_partial(DevParams p, const u64* __restrict__ ct, const u32* __restrict__ perm, int c0, PermGemm g,
-                  const int* __restrict__ D, u64* __restrict__ part) {
+                  const u64* __restrict__ V, u64* __restrict__ part) {
   constexpr int TPB = 256;
   const int N = p.N, cl = blockIdx.x, h = blockIdx.y, sl = blockIdx.z, tid = threadIdx.x;
   const int c = c0 + cl;
@@ -580,15 +570,12 @@ k_permute_partial(DevParams p, const u64* __restrict__ ct, const u32* __restrict
   for (int i = 1 + sl * per; i <= (sl + 1) * per; i++) {
     int j = (int)perm[(size_t)c * N + (i - 1)];
     if (j < 1 || j > N || j == i) continue;                      // uniform across the CTA
-    const int* drow = D + ((size_t)cl * N + (i - 1)) * g.Nout + (size_t)h * N;
+    const u64* vrow = V + ((size_t)cl * N + (i - 1)) * 2 * N + (size_t)h * N;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < CPT; r++) {
       const int x = tid + r * TPB;
-      u64 v = 0;                                                  // sum_l digit_l 256^l mod Q
-#pragma unroll
-      for (int l = 6; l >= 0; l--) v = horner_mod(v, 8, drow[(size_t)l * 2 * N + x], p);
-      u64 t = neg_mod(v, Q);                                      // -W_i
+      u64 t = neg_mod(__ldg(vrow + x), Q);                        // -W_i
       if (h == 0 && x == 0) t = add_mod(t, sub_mod(cth[j - 1], cth[i - 1], Q), Q);   // + [b_j - b_i, 0]
       W[x] = t;
     }

@@ -44,7 +44,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_pack", "fdfb_device_status", "fdfb_key_export", "fdfb_shift_streaming",
             "fdfb_workspace_keyswitch", "fdfb_workspace_bootstrap_multi", "fdfb_bootstrap_multi_batch",
             "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute",
-            "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch", "fdfb_lwe_decrypt", "fdfb_rlwe_phase"]
+            "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch", "fdfb_lwe_decrypt", "fdfb_rlwe_phase",
+            "fdfb_gemm_i8"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -101,6 +102,7 @@ def lib():
         L.fdfb_shift.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_shift_streaming.argtypes = [vp, vp, vp, vp, vp, u32, vp]
         L.fdfb_poly_mul.argtypes = [vp, vp, vp, vp, u32, vp]
+        L.fdfb_gemm_i8.argtypes = [vp, vp, vp, u32, u32, u32, vp, vp]
         L.fdfb_cdt_table.argtypes = [vp, vp, C.POINTER(C.c_int)]
         L.fdfb_launch_count.argtypes = [vp]
         L.fdfb_launch_count.restype = u64
@@ -389,6 +391,14 @@ class Context:
         out = torch.empty_like(a)
         _check(lib().fdfb_poly_mul(self.h, _ptr(a), _ptr(b), _ptr(out), a.shape[0], _stream(stream)))
         return out
+
+    def gemm_i8(self, A, B, stream=None):
+        """D = A @ B.T exactly (int8 x int8 -> int32) on the tcgen05 kernel (fdfb_gemm_i8)."""
+        M, K = A.shape
+        Nc = B.shape[0]
+        D = torch.empty((M, Nc), dtype=torch.int32, device=self.device)
+        _check(lib().fdfb_gemm_i8(self.h, _ptr(A), _ptr(B), M, Nc, K, _ptr(D), _stream(stream)))
+        return D
 
     def cdt_table(self):
         import numpy as np
