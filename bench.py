@@ -237,8 +237,9 @@ class BootstrapWorkload:
         self.rotp = ctx.setup_lut(self.f)
         start, count = shard_range(B * world, world, rank)
         self.msgs = synth.messages(cfg, B * world)[start:start + count]
-        self.ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"] + rank, keys["s"],
-                                     torch.from_numpy(self.msgs.copy()).to(dev))
+        # global object indices: a shard encrypts exactly what one device would for the whole batch
+        self.ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"], keys["s"], torch.from_numpy(self.msgs.copy()).to(dev),
+                                     first_index=start)
         self.ct_out = torch.empty_like(self.ct_in)
         self.ws = ctx.workspace_bootstrap(B)
         self.io_bytes = B * (ctx.n + 1) * 8
@@ -300,7 +301,7 @@ class ShiftWorkload:
     metric = "shifts/sec (N=2048, L_pK=2, ell_pK=54)"
     unit = "shifts/s"
     kclass = ("shift", "shift_gemm")
-    kernel = "k_shift_bits + cuBLASLt int8 GEMM + k_shift_gemm_finish"
+    kernel = "k_shift_bits + k_imma<2> (tcgen05 int8 GEMM, recombining epilogue) + k_shift_gemm_finish"
 
     def __init__(self, ctx, cfg, B, rank, world, dev, stream):
         import torch
@@ -325,7 +326,8 @@ class ShiftWorkload:
         start, count = shard_range(B * world, world, rank)
         self.msg = synth.rlwe_messages(cfg, B * world)[start:start + count]
         self.d = synth.shift_amounts(cfg, B * world)[start:start + count]
-        self.ct_in = ctx.rlwe_encrypt(cfg["seeds"]["err"] + rank, keys["S"], torch.from_numpy(self.msg).to(dev))
+        self.ct_in = ctx.rlwe_encrypt(cfg["seeds"]["err"], keys["S"], torch.from_numpy(self.msg).to(dev),
+                                      first_index=start)
         self.d_dev = torch.from_numpy(self.d.astype("uint32")).to(dev)
         self.ct_out = torch.empty_like(self.ct_in)
         self.ws = ctx.workspace_shift(B)
@@ -495,7 +497,7 @@ class PermuteWorkload(ShiftWorkload):
     """fdfb_permute over B RLWE ciphertexts with uniformly random permutations (Shift config keys)."""
     metric = "permutes/sec (N=2048, L_pK=2, ell_pK=54)"
     unit = "permutes/s"
-    kernel = "k_perm_bits + cuBLASLt int8 GEMM + k_permute_finish"
+    kernel = "k_perm_bits + k_imma<2> (tcgen05 int8 GEMM) + k_permute_partial/reduce"
 
     def __init__(self, ctx, cfg, B, rank, world, dev, stream):
         import numpy as np
@@ -551,7 +553,7 @@ class ShiftBootWorkload:
     metric = "shift-based bootstraps/sec (N=2048, L_pK=2)"
     unit = "bootstraps/s"
     kclass = "shift_gemm"
-    kernel = "cuBLASLt int8 GEMM (Shift inside every CMux)"
+    kernel = "k_imma<2> tcgen05 int8 GEMM (Shift inside every CMux)"
 
     def __init__(self, ctx, cfg, B, rank, world, dev, stream):
         import numpy as np
@@ -582,8 +584,9 @@ class ShiftBootWorkload:
         self.rotp = torch.from_numpy(np.array([(delta * int(v)) % Q for v in self.g], np.uint64)).to(dev)
         start, count = shard_range(B * world, world, rank)
         self.msgs = synth.messages(cfg, B * world)[start:start + count]
-        self.ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"] + rank, keys["s"],
-                                     torch.from_numpy(self.msgs.copy()).to(dev))
+        # global object indices: a shard encrypts exactly what one device would for the whole batch
+        self.ct_in = ctx.lwe_encrypt(cfg["seeds"]["err"], keys["s"], torch.from_numpy(self.msgs.copy()).to(dev),
+                                     first_index=start)
         self.ct_out = torch.empty_like(self.ct_in)
         self.ws = ctx.workspace_bootstrap_shift(B)
         self.io_bytes = B * (ctx.n + 1) * 8

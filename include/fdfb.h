@@ -109,30 +109,40 @@ size_t fdfb_workspace_vector_pack(const fdfb_ctx* ctx, uint32_t m, uint32_t B);
  * for pK and ksK (2369-2371, 2992-3001), PackSetup (1284-1296).  which: bitmask
  * 1=secrets 2=brk 4=bpk 8=ksk 16=pack; pointers of unselected keys may be NULL,
  * but brk/bpk/ksk/pack need the secrets in sk_lwe/sk_rlwe [dev] (generated in the
- * same call if bit 1 is set).  Allocates and frees device temporaries; syncs. */
+ * same call if bit 1 is set).  workspace [dev] of fdfb_workspace_keygen(ctx) bytes (may be
+ * NULL when only secrets are generated; FDFB_E_WORKSPACE otherwise).  Syncs.  Like every
+ * entry point, it allocates no device memory (all scratch comes from the caller). */
+size_t fdfb_workspace_keygen(const fdfb_ctx* ctx);
 int fdfb_keygen(const fdfb_ctx* ctx, uint64_t seed, uint32_t which, int8_t* sk_lwe, int8_t* sk_rlwe,
-                void* brk, void* bpk, void* ksk, void* pack, void* stream);
+                void* brk, void* bpk, void* ksk, void* pack, void* workspace, void* stream);
 /* Canonical key entries for parity checks: `count` entries with flat canonical entry
  * indices idx[] [host] (BRK: (i*u+j)*2ell+row; BPK/KSK: i*ell+j; PACK: (i*ell+j)*L+k),
- * written back to back into out [dev] (2N words per RLWE entry, n+1 per LWE entry). */
+ * written back to back into out [dev] (2N words per RLWE entry, n+1 per LWE entry).
+ * workspace [dev] of fdfb_workspace_keygen_canonical(ctx, count) bytes.  Syncs. */
+size_t fdfb_workspace_keygen_canonical(const fdfb_ctx* ctx, uint32_t count);
 int fdfb_keygen_canonical(const fdfb_ctx* ctx, uint64_t seed, int kind, const int8_t* sk_lwe,
                           const int8_t* sk_rlwe, const uint64_t* idx, uint32_t count, uint64_t* out,
-                          void* stream);
+                          void* workspace, void* stream);
 /* Convert a canonical key [dev] to the opaque device format [dev].  Syncs. */
 int fdfb_key_import(const fdfb_ctx* ctx, int kind, const uint64_t* canonical, void* dev_key, void* stream);
 
-/* Canonical layout of a device key [dev] -> canonical [dev] (BPK, KSK, PACK; BRK is
- * held only in the NTT domain and returns FDFB_E_UNSUPPORTED).  Stream-ordered. */
+/* Canonical layout of a device key [dev] -> canonical [dev] (all kinds; BRK, held only as
+ * RNS residues in the NTT domain, is brought back by inverse NTTs and the CRT -- exact, since
+ * every canonical coefficient is below Q < P).  Stream-ordered. */
 int fdfb_key_export(const fdfb_ctx* ctx, int kind, const void* dev_key, uint64_t* canonical, void* stream);
 
 /* ------------------------------------------------------------------ inputs
- * LWE encryptions of m[c] in Z_t (Delta = q_lwe/t) under sk_lwe,
- * object c of domain 7.  flags bit0: mod-switch-exact inputs. */
+ * LWE encryptions of m[c] in Z_t (Delta = q_lwe/t) under sk_lwe, c = 0 ..
+ * count-1 -> out[c], drawn as object first_index + c of domain 7 (a shard of a global batch
+ * passes its global offset and encrypts exactly what one device would).  flags bit0:
+ * mod-switch-exact inputs. */
 int fdfb_lwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_lwe, const uint64_t* msg,
-                     uint32_t count, uint32_t flags, uint64_t* out, void* stream);
-/* RLWE encryptions of message polynomials msg [dev, count x N] (domain 8). */
+                     uint32_t count, uint32_t flags, uint64_t first_index, uint64_t* out, void* stream);
+/* RLWE encryptions of message polynomials msg [dev, count x N] (domain 8, objects
+ * first_index + c).  workspace [dev] of fdfb_workspace_rlwe_encrypt(ctx, count) bytes. */
+size_t fdfb_workspace_rlwe_encrypt(const fdfb_ctx* ctx, uint32_t count);
 int fdfb_rlwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_rlwe, const uint64_t* msg,
-                      uint32_t count, uint64_t* out, void* stream);
+                      uint32_t count, uint64_t first_index, uint64_t* out, void* workspace, void* stream);
 
 /* ------------------------------------------------------------------ decryption (secret-key side)
  * Phase of LWE ciphertexts ct [dev, count x (n+1)] mod q_lwe under sk_lwe [dev, n int8]:
@@ -142,9 +152,11 @@ int fdfb_rlwe_encrypt(const fdfb_ctx* ctx, uint64_t seed, const int8_t* sk_rlwe,
 int fdfb_lwe_decrypt(const fdfb_ctx* ctx, const int8_t* sk_lwe, const uint64_t* ct, uint32_t count, uint32_t t,
                      uint64_t* phase, uint64_t* msg, void* stream);
 /* Phase of RLWE ciphertexts ct [dev, count x 2 x N] under sk_rlwe [dev, N int8]:
- * out = b - a * s mod Q (negacyclic product) [dev, count x N]. */
+ * out = b - a * s mod Q (negacyclic product) [dev, count x N].
+ * workspace [dev] of fdfb_workspace_rlwe_phase(ctx, count) bytes. */
+size_t fdfb_workspace_rlwe_phase(const fdfb_ctx* ctx, uint32_t count);
 int fdfb_rlwe_phase(const fdfb_ctx* ctx, const int8_t* sk_rlwe, const uint64_t* ct, uint32_t count, uint64_t* out,
-                    void* stream);
+                    void* workspace, void* stream);
 
 /* ------------------------------------------------------------------ LUT
  * BootsMap[x] = round(Q/t_out) * lut[x] then SetupPolynomial
@@ -247,9 +259,10 @@ int fdfb_shift_streaming(const fdfb_ctx* ctx, const void* pack, const uint64_t* 
 
 /* ------------------------------------------------------------------ kernel unit tests
  * Negacyclic ring product through the NTT kernels: c = a * b mod (X^N+1, Q),
- * a, b, c [dev, count x N]. */
+ * a, b, c [dev, count x N]; workspace [dev] of fdfb_workspace_poly_mul(ctx, count) bytes. */
+size_t fdfb_workspace_poly_mul(const fdfb_ctx* ctx, uint32_t count);
 int fdfb_poly_mul(const fdfb_ctx* ctx, const uint64_t* a, const uint64_t* b, uint64_t* c, uint32_t count,
-                  void* stream);
+                  void* workspace, void* stream);
 /* The int8 tensor-core contraction under both key switches, Shift and Permute
  * (kernels_imma.cuh: TMA loads, tcgen05.mma kind::i8, int32 accumulators in TMEM), with its
  * raw epilogue: D [dev, M x Ncols] int32 = A [dev, M x K] int8 (K-major) x B [dev, Ncols x K]

@@ -37,6 +37,7 @@ struct fdfb_ctx {
   mutable bool timing = false;
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
   int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 batched only, 1 auto (default), 2 / 3 force clusters of NP / 2 NP
+  int imma_cg = 2;           // FDFB_IMMA_CG: int8 GEMM tiles per CTA pair (2, default) or per CTA (1)
 };
 
 // Bracket one launch of kernel class `cls` with events on its stream when timing is on.
@@ -57,7 +58,7 @@ static thread_local std::string g_last_cuda;
 struct PackLayout;
 static size_t shift_pack_bytes(const fdfb_params& p);
 static int pack_keygen(const fdfb_ctx* c, u64 seed, const int8_t* s_rlwe, void* pack, u64* shat, u64* tmask,
-                       u64* tprod, u64* tout, int CH, cudaStream_t st);
+                       u64* tprod, int CH, cudaStream_t st);
 static int pack_import(const fdfb_ctx* c, const u64* canon, void* dev, cudaStream_t st);
 
 #define CK(x)                                                              \
@@ -109,8 +110,8 @@ static u64 shoup_of(u64 w, u64 Q) { return (u64)(((u128)w << 64) / Q); }
 static int bitrev(int x, int logn) { int r = 0; for (int i = 0; i < logn; i++) r |= ((x >> i) & 1) << (logn - 1 - i); return r; }
 
 // Library-side CDT (reading G17): the thresholds floor(2^64 CDF(-T + k)) for sigma = 3.2 are
-// data, generated once with exact fixed-point arithmetic by tools/gen_cdt_table.py (independent
-// of the oracle's table code); sigma_milli = 0 means noiseless keys, other sigmas are rejected.
+// data, generated once with exact fixed-point arithmetic by tools/gen_cdt_table.py (its own
+// derivation, shared with no test code); sigma_milli = 0 means noiseless keys, other sigmas are rejected.
 #include "cdt_table.inc"
 static bool make_cdt(uint32_t sigma_milli, std::vector<u64>* thr, int* Tout) {
   thr->clear();
@@ -316,22 +317,42 @@ static int make_tmap_i8(CUtensorMap* m, const void* base, size_t rows, size_t K,
   return FDFB_OK;
 }
 // D = A [M][K] (pitch lda) x B [Ncols][K]^T (pitch ldb), both int8 K-major, through the
-// epilogue e (kernels_imma.cuh); Ncols is a multiple of imma::BN except in raw mode.
+// epilogue e (kernels_imma.cuh); Ncols is a multiple of imma::BN except in raw mode.  CTA pairs
+// (cta_group::2, 256-row tiles) unless FDFB_IMMA_CG=1.
+template <int CG>
+static int imma_launch(const fdfb_ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, size_t M, size_t Ncols,
+                       size_t K, const ImmaEpi& e, int kclass, cudaStream_t st) {
+  const int tiles_m = (int)((M + imma::BM * CG - 1) / (imma::BM * CG));
+  const int tiles_n = (int)((Ncols + imma::BN - 1) / imma::BN);
+  const long long nt = (long long)tiles_m * tiles_n;
+  const int units = (int)(nt < c->num_sms / CG ? nt : c->num_sms / CG);
+  const size_t smem = imma::Cfg<CG>::SMEM;
+  CK(cudaFuncSetAttribute(k_imma<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(imma::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = CG; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  TimedLaunch tl(c, kclass, st);
+  CK(cudaLaunchKernelEx(&cfg, k_imma<CG>, ta, tb, (int)K, tiles_m, tiles_n, c->dp, e));
+  CKL(c);
+  return FDFB_OK;
+}
 static int imma_gemm(const fdfb_ctx* c, const int8_t* A, size_t M, size_t lda, const int8_t* B, size_t Ncols,
                      size_t ldb, size_t K, const ImmaEpi& e, int kclass, cudaStream_t st) {
   if (M == 0) return FDFB_OK;
+  const int cg = c->imma_cg;
   CUtensorMap ta, tb;
   int rc = make_tmap_i8(&ta, A, M, K, lda, imma::BM);
-  if (!rc) rc = make_tmap_i8(&tb, B, Ncols, K, ldb, imma::BN);
+  if (!rc) rc = make_tmap_i8(&tb, B, Ncols, K, ldb, imma::BN / cg);
   if (rc) return rc;
-  const int tiles_m = (int)((M + imma::BM - 1) / imma::BM), tiles_n = (int)((Ncols + imma::BN - 1) / imma::BN);
-  const long long nt = (long long)tiles_m * tiles_n;
-  const int grid = (int)(nt < c->num_sms ? nt : c->num_sms);
-  CK(cudaFuncSetAttribute(k_imma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)imma::SMEM));
-  TimedLaunch tl(c, kclass, st);
-  k_imma<<<grid, imma::THREADS, imma::SMEM, st>>>(ta, tb, (int)K, tiles_m, tiles_n, c->dp, e);
-  CKL(c);
-  return FDFB_OK;
+  return cg == 2 ? imma_launch<2>(c, ta, tb, M, Ncols, K, e, kclass, st)
+                 : imma_launch<1>(c, ta, tb, M, Ncols, K, e, kclass, st);
 }
 
 // ------------------------------------------------------------------ key switching
@@ -467,8 +488,16 @@ static u64 h_primroot_2n(u64 pr, int N) {
   }
   return 0;
 }
-// Choose the RNS primes (largest p < 2^28 so that 16p < 2^32, p = 1 mod 2N) so that prod p > 2 * bound + 1 with
-// bound = 2 ell N (L-1) (Q-1) >= |coefficients| of sum_r D_r * K_r; build constants/tables.
+// The kernel rounds k = floor((sum_i f_i + 8) / 16) with f_i = floor(16 t_i / p_i) - {0, 1}
+// (and f16's truncation, < 1/16 each): sum f_i lies in [16 X - 17 NP / 16, 16 X] for
+// X = sum t_i / p_i = k + V / P, |V| <= bound.  k is exact iff 16 bound / P + 17 NP / 16 <= 8
+// (lower side) and 16 bound / P < 8 (upper side), i.e. 256 bound + 17 NP P <= 128 P.
+static bool crt_rounding_exact(u128 bound, u128 P, int np) {
+  return (u128)256 * bound + (u128)17 * np * P <= (u128)128 * P;
+}
+// Choose the RNS primes (largest p < 2^28 so that 16p < 2^32, p = 1 mod 2N) until the CRT
+// rounding is exact for bound = 2 ell N (L-1) (Q-1) >= |coefficients| of sum_r D_r * K_r; build
+// constants/tables.
 static int setup_rns(fdfb_ctx* c) {
   const fdfb_params& p = c->prm;
   const int N = p.N;
@@ -489,10 +518,25 @@ static int setup_rns(fdfb_ctx* c) {
       if (cand >= (1ULL << 28) || cand == p.Q || !h_is_prime(cand)) continue;
       primes.push_back(cand);
       P *= cand;
-      if (primes.size() >= 2 && P / 8 * 3 > bound + 1) break;
+      if (primes.size() >= 2 && crt_rounding_exact(bound, P, (int)primes.size())) break;
     }
-    // |V| <= bound < 3P/8 keeps sum_i t_i / p_i within 1/8 of an integer (the kernel's CRT rounding)
-    if (primes.size() < 2 || P / 8 * 3 <= bound + 1) return FDFB_E_UNSUPPORTED;
+    if (primes.size() < 2 || !crt_rounding_exact(bound, P, (int)primes.size())) return FDFB_E_UNSUPPORTED;
+  }
+  // MAC range of k_blind_rotate: 2 ell products of forward outputs (< B p, B = fwd_out_bound)
+  // and key residues (< p) plus the Montgomery term stay below 2^64, and the reduced value
+  // below 16p (three conditional subtractions then reach [0, 2p))
+  {
+    int B = 16;
+    switch (N) {
+      case 256: B = fwd_out_bound<256>(); break;
+      case 512: B = fwd_out_bound<512>(); break;
+      case 1024: B = fwd_out_bound<1024>(); break;
+      default: B = fwd_out_bound<2048>(); break;
+    }
+    for (u64 pr : primes) {
+      const u128 smax = (u128)(2 * p.ell_rgsw) * B * pr * pr + (u128)0xFFFFFFFFull * pr;
+      if (smax >= ((u128)1 << 64) || (u64)(smax >> 32) >= 16 * pr) return FDFB_E_UNSUPPORTED;
+    }
   }
   R.np = (int)primes.size();
   const u64 Q = p.Q;
@@ -580,6 +624,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
   if ((rc = setup_rns(c))) { delete c; return rc; }
   if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
+  if (const char* e = getenv("FDFB_IMMA_CG")) c->imma_cg = atoi(e) == 1 ? 1 : 2;
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));
   d.Q = Q; d.Q2 = 2 * Q; d.Q4 = 4 * Q; d.half = (Q + 1) / 2;
@@ -722,7 +767,7 @@ static int brk_rns_t(const fdfb_ctx* c, const u64* canon, size_t rows, size_t ro
   CKL(c);
   return FDFB_OK;
 }
-static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, size_t row0, u64* dev, u64* /*tmp*/,
+static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, size_t row0, u64* dev,
                            cudaStream_t st) {
   switch (c->prm.N) {
     case 256: return brk_rns_t<256>(c, canon, rows, row0, (u32*)dev, st);
@@ -733,8 +778,27 @@ static int brk_import_rows(const fdfb_ctx* c, const u64* canon, size_t rows, siz
   return FDFB_E_DIMENSION;
 }
 
+// keygen scratch: the ring secret's NTT, and per chunk of CH RLWE entries the mask, the mask
+// product and the encrypted entries
+static const int kKeygenChunk = 2048;
+struct KeygenWs { u64* shat; u64* tmask; u64* tprod; u64* tout; size_t bytes; };
+static KeygenWs keygen_ws(const fdfb_params& p, void* base) {
+  KeygenWs w;
+  char* b = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = b + off; off += (bytes + 255) & ~(size_t)255; return r; };
+  const size_t N = p.N, CH = kKeygenChunk;
+  w.shat = (u64*)take(N * 8);
+  w.tmask = (u64*)take(CH * N * 8);
+  w.tprod = (u64*)take(CH * N * 8);
+  w.tout = (u64*)take(CH * 2 * N * 8);
+  w.bytes = off;
+  return w;
+}
+extern "C" size_t fdfb_workspace_keygen(const fdfb_ctx* c) { return c ? keygen_ws(c->prm, nullptr).bytes : 0; }
+
 extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int8_t* sk_lwe, int8_t* sk_rlwe,
-                           void* brk, void* bpk, void* ksk, void* pack, void* stream) {
+                           void* brk, void* bpk, void* ksk, void* pack, void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   cudaStream_t st = S(stream);
   const fdfb_params& p = c->prm;
@@ -742,32 +806,30 @@ extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int
   if (!sk_lwe || !sk_rlwe) return FDFB_E_NULL;
   if (((which & 2) && !brk) || ((which & 4) && !bpk) || ((which & 8) && !ksk) || ((which & 16) && !pack))
     return FDFB_E_NULL;
+  if ((which & 30) && !workspace) return FDFB_E_WORKSPACE;
   if (which & 1) {
     int m = p.n > p.N ? p.n : p.N;
     k_keygen_secrets<<<(m + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe);
     CKL(c);
   }
-  const int CH = 2048;  // RLWE entries per chunk
-  u64 *shat = nullptr, *tmask = nullptr, *tprod = nullptr, *tout = nullptr, *tntt = nullptr;
-  CK(cudaMallocAsync(&shat, (size_t)N * 8, st));
-  CK(cudaMallocAsync(&tmask, (size_t)CH * N * 8, st));
-  CK(cudaMallocAsync(&tprod, (size_t)CH * N * 8, st));
-  CK(cudaMallocAsync(&tout, (size_t)CH * 2 * N * 8, st));
-  CK(cudaMallocAsync(&tntt, (size_t)CH * 2 * N * 8, st));
-  int rc = make_shat(c, sk_rlwe, shat, st);
+  if (!(which & 30)) { CK(cudaStreamSynchronize(st)); return FDFB_OK; }
+  const int CH = kKeygenChunk;  // RLWE entries per chunk
+  KeygenWs w = keygen_ws(p, workspace);
+  int rc = make_shat(c, sk_rlwe, w.shat, st);
   if (!rc && (which & 2)) {
     size_t rows = brk_words(p) / (2 * (size_t)N);
     for (size_t o = 0; o < rows && !rc; o += CH) {
       int cnt = (int)((rows - o) < (size_t)CH ? (rows - o) : CH);
-      rc = rlwe_entries(c, seed, 1, sk_lwe, sk_rlwe, nullptr, o, cnt, tout, shat, tmask, tprod, st);
-      if (!rc) rc = brk_import_rows(c, tout, cnt, o, (u64*)brk, tntt, st);
+      rc = rlwe_entries(c, seed, 1, sk_lwe, sk_rlwe, nullptr, o, cnt, w.tout, w.shat, w.tmask, w.tprod, st);
+      if (!rc) rc = brk_import_rows(c, w.tout, cnt, o, (u64*)brk, st);
     }
   }
   if (!rc && (which & 4)) {
     size_t ent = (size_t)N * p.ell_pk;
     for (size_t o = 0; o < ent && !rc; o += CH) {
       int cnt = (int)((ent - o) < (size_t)CH ? (ent - o) : CH);
-      rc = rlwe_entries(c, seed, 2, sk_lwe, sk_rlwe, nullptr, o, cnt, (u64*)bpk + o * 2 * N, shat, tmask, tprod, st);
+      rc = rlwe_entries(c, seed, 2, sk_lwe, sk_rlwe, nullptr, o, cnt, (u64*)bpk + o * 2 * N, w.shat, w.tmask,
+                        w.tprod, st);
     }
     if (!rc) rc = ks_build_key(c, (const u64*)bpk, canon_bpk_bytes(p), ks_shape_rlwe(p), 0, bpk, st);
   }
@@ -777,42 +839,44 @@ extern "C" int fdfb_keygen(const fdfb_ctx* c, uint64_t seed, uint32_t which, int
     CKL(c);
     rc = ks_build_key(c, (const u64*)ksk, canon_ksk_bytes(p), ks_shape_lwe(p), (int)p.log_q_lwe, ksk, st);
   }
-  if (!rc && (which & 16)) rc = pack_keygen(c, seed, sk_rlwe, pack, shat, tmask, tprod, tout, CH, st);
-  cudaFreeAsync(shat, st); cudaFreeAsync(tmask, st); cudaFreeAsync(tprod, st); cudaFreeAsync(tout, st);
-  cudaFreeAsync(tntt, st);
+  if (!rc && (which & 16)) rc = pack_keygen(c, seed, sk_rlwe, pack, w.shat, w.tmask, w.tprod, CH, st);
   if (rc) return rc;
   CK(cudaStreamSynchronize(st));
   return FDFB_OK;
 }
 
+// keygen_canonical scratch: the entry indices, the ring secret's NTT, mask and mask product
+static size_t keycanon_ws_bytes(const fdfb_params& p, uint32_t count) {
+  return align256((size_t)count * 8) + align256((size_t)p.N * 8) + 2 * align256((size_t)count * p.N * 8);
+}
+extern "C" size_t fdfb_workspace_keygen_canonical(const fdfb_ctx* c, uint32_t count) {
+  return c ? keycanon_ws_bytes(c->prm, count) : 0;
+}
 extern "C" int fdfb_keygen_canonical(const fdfb_ctx* c, uint64_t seed, int kind, const int8_t* sk_lwe,
                                      const int8_t* sk_rlwe, const uint64_t* idx, uint32_t count, uint64_t* out,
-                                     void* stream) {
+                                     void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (count == 0) return FDFB_OK;  // empty batch: data pointers may be NULL
   if (!idx || !out || !sk_lwe || !sk_rlwe) return FDFB_E_NULL;
+  if (kind != FDFB_KEY_KSK && kind != FDFB_KEY_BRK && kind != FDFB_KEY_BPK && kind != FDFB_KEY_PACK) return FDFB_E_KIND;
+  if (!workspace) return FDFB_E_WORKSPACE;
   cudaStream_t st = S(stream);
   const int N = c->prm.N;
-  u64* didx = nullptr;
-  CK(cudaMallocAsync(&didx, (size_t)count * 8, st));
+  char* b = (char*)workspace;
+  u64* didx = (u64*)b;
+  u64* shat = (u64*)(b + align256((size_t)count * 8));
+  u64* tm = (u64*)((char*)shat + align256((size_t)N * 8));
+  u64* tp = (u64*)((char*)tm + align256((size_t)count * N * 8));
   CK(cudaMemcpyAsync(didx, idx, (size_t)count * 8, cudaMemcpyHostToDevice, st));
   int rc = FDFB_OK;
   if (kind == FDFB_KEY_KSK) {
     k_ksk_gen<<<(count * 32 + 255) / 256, 256, 0, st>>>(c->dp, seed, sk_lwe, sk_rlwe, didx, 0, count, out);
     CKL(c);
-  } else if (kind == FDFB_KEY_BRK || kind == FDFB_KEY_BPK || kind == FDFB_KEY_PACK) {
-    u64 *shat, *tm, *tp;
-    CK(cudaMallocAsync(&shat, (size_t)N * 8, st));
-    CK(cudaMallocAsync(&tm, (size_t)count * N * 8, st));
-    CK(cudaMallocAsync(&tp, (size_t)count * N * 8, st));
+  } else {
     rc = make_shat(c, sk_rlwe, shat, st);
     int k = kind == FDFB_KEY_BRK ? 1 : (kind == FDFB_KEY_BPK ? 2 : 3);
     if (!rc) rc = rlwe_entries(c, seed, k, sk_lwe, sk_rlwe, didx, 0, count, out, shat, tm, tp, st);
-    cudaFreeAsync(shat, st); cudaFreeAsync(tm, st); cudaFreeAsync(tp, st);
-  } else {
-    rc = FDFB_E_KIND;
   }
-  cudaFreeAsync(didx, st);
   if (rc) return rc;
   CK(cudaStreamSynchronize(st));
   return FDFB_OK;
@@ -828,13 +892,10 @@ extern "C" int fdfb_key_import(const fdfb_ctx* c, int kind, const uint64_t* cano
   if (kind == FDFB_KEY_BRK) {
     size_t rows = brk_words(p) / (2 * (size_t)p.N);
     const size_t CH = 4096;
-    u64* tmp;
-    CK(cudaMallocAsync(&tmp, CH * 2 * p.N * 8, st));
     for (size_t o = 0; o < rows && !rc; o += CH) {
       size_t cnt = (rows - o) < CH ? (rows - o) : CH;
-      rc = brk_import_rows(c, canon + o * 2 * p.N, cnt, o, (u64*)dev_key, tmp, st);
+      rc = brk_import_rows(c, canon + o * 2 * p.N, cnt, o, (u64*)dev_key, st);
     }
-    cudaFreeAsync(tmp, st);
   } else if (kind == FDFB_KEY_BPK) {
     rc = ks_build_key(c, canon, sz.canon_bpk, ks_shape_rlwe(p), 0, dev_key, st);
   } else if (kind == FDFB_KEY_KSK) {
@@ -849,43 +910,83 @@ extern "C" int fdfb_key_import(const fdfb_ctx* c, int kind, const uint64_t* cano
   return FDFB_OK;
 }
 
+template <int N>
+static int brk_export_t(const fdfb_ctx* c, const u32* dev, u64* canon, size_t rows, cudaStream_t st) {
+  const RnsParams& R = c->rns;
+  BrkExportC X;
+  memset(&X, 0, sizeof(X));
+  u128 P = 1;
+  for (int i = 0; i < R.np; i++) P *= R.p[i];
+  for (int i = 0; i < R.np; i++) {
+    const u64 pr = R.p[i];
+    X.inv32[i] = (u32)h_inv((1ULL << 32) % pr, pr);
+    X.inv32s[i] = (u32)(((u64)X.inv32[i] << 32) / pr);
+    X.Pi[i] = (u64)(P / pr);
+  }
+  X.P_lo = (u64)P; X.P_hi = (u64)(P >> 64);
+  const size_t CH = 1 << 20;                        // polynomials per launch
+  for (size_t o = 0; o < 2 * rows; o += CH) {
+    const size_t cnt = (2 * rows - o) < CH ? (2 * rows - o) : CH;
+    k_brk_export<N><<<(unsigned)cnt, N / 8, 0, st>>>(c->dp, R, X, dev, o / 2, canon);
+    CKL(c);
+  }
+  return FDFB_OK;
+}
 extern "C" int fdfb_key_export(const fdfb_ctx* c, int kind, const void* dev_key, uint64_t* canon, void* stream) {
   if (!c || !dev_key || !canon) return FDFB_E_NULL;
   fdfb_sizes_t sz;
   fdfb_sizes(c, &sz);
+  if (kind == FDFB_KEY_BRK) {                        // inverse RNS NTT + CRT (k_brk_export)
+    const size_t rows = brk_words(c->prm) / (2 * (size_t)c->prm.N);
+    const u32* d = (const u32*)dev_key;
+    switch (c->prm.N) {
+      case 256: return brk_export_t<256>(c, d, canon, rows, S(stream));
+      case 512: return brk_export_t<512>(c, d, canon, rows, S(stream));
+      case 1024: return brk_export_t<1024>(c, d, canon, rows, S(stream));
+      case 2048: return brk_export_t<2048>(c, d, canon, rows, S(stream));
+    }
+    return FDFB_E_DIMENSION;
+  }
   size_t bytes = kind == FDFB_KEY_BPK ? sz.canon_bpk : kind == FDFB_KEY_KSK ? sz.canon_ksk
                : kind == FDFB_KEY_PACK ? sz.canon_pack : 0;
-  if (kind == FDFB_KEY_BRK) return FDFB_E_UNSUPPORTED;
   if (!bytes) return FDFB_E_KIND;
   CK(cudaMemcpyAsync(canon, dev_key, bytes, cudaMemcpyDeviceToDevice, S(stream)));
   return FDFB_OK;
 }
 
 extern "C" int fdfb_lwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_lwe, const uint64_t* msg,
-                                uint32_t count, uint32_t flags, uint64_t* out, void* stream) {
+                                uint32_t count, uint32_t flags, uint64_t first_index, uint64_t* out, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
   if (!sk_lwe || !msg || !out) return FDFB_E_NULL;
-  k_lwe_encrypt<<<((size_t)count * 32 + 255) / 256, 256, 0, S(stream)>>>(c->dp, seed, sk_lwe, msg, count, flags, out);
+  k_lwe_encrypt<<<((size_t)count * 32 + 255) / 256, 256, 0, S(stream)>>>(c->dp, seed, sk_lwe, msg, count, flags,
+                                                                          first_index, out);
   CKL(c);
   return FDFB_OK;
 }
 
+// rlwe_encrypt scratch: the ring secret's NTT, the masks and their products with the secret
+static size_t rlwe_enc_ws_bytes(const fdfb_params& p, uint32_t count) {
+  return align256((size_t)p.N * 8) + 2 * align256((size_t)count * p.N * 8);
+}
+extern "C" size_t fdfb_workspace_rlwe_encrypt(const fdfb_ctx* c, uint32_t count) {
+  return c ? rlwe_enc_ws_bytes(c->prm, count) : 0;
+}
 extern "C" int fdfb_rlwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t* sk_rlwe, const uint64_t* msg,
-                                 uint32_t count, uint64_t* out, void* stream) {
+                                 uint32_t count, uint64_t first_index, uint64_t* out, void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
   if (!sk_rlwe || !msg || !out) return FDFB_E_NULL;
+  if (!workspace) return FDFB_E_WORKSPACE;
   cudaStream_t st = S(stream);
   const int N = c->prm.N;
-  u64 *shat, *tm, *tp;
-  CK(cudaMallocAsync(&shat, (size_t)N * 8, st));
-  CK(cudaMallocAsync(&tm, (size_t)count * N * 8, st));
-  CK(cudaMallocAsync(&tp, (size_t)count * N * 8, st));
+  u64* shat = (u64*)workspace;
+  u64* tm = (u64*)((char*)shat + align256((size_t)N * 8));
+  u64* tp = (u64*)((char*)tm + align256((size_t)count * N * 8));
   int rc = make_shat(c, sk_rlwe, shat, st);
   dim3 g1((N + 255) / 256, count);
   if (!rc) {
-    k_rlwe_enc_mask<<<g1, 256, 0, st>>>(c->dp, seed, count, tm);
+    k_rlwe_enc_mask<<<g1, 256, 0, st>>>(c->dp, seed, count, first_index, tm);
     CKL(c);
     CK(cudaMemcpyAsync(tp, tm, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
     rc = launch_ntt_batch(c, tp, count, 0, st);
@@ -897,10 +998,9 @@ extern "C" int fdfb_rlwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t*
     rc = launch_ntt_batch(c, tp, count, 1, st);
   }
   if (!rc) {
-    k_rlwe_enc_finish<<<g1, 256, 0, st>>>(c->dp, seed, count, msg, tm, tp, out);
+    k_rlwe_enc_finish<<<g1, 256, 0, st>>>(c->dp, seed, count, first_index, msg, tm, tp, out);
     CKL(c);
   }
-  cudaFreeAsync(shat, st); cudaFreeAsync(tm, st); cudaFreeAsync(tp, st);
   return rc;
 }
 
@@ -1111,15 +1211,18 @@ extern "C" int fdfb_lwe_keyswitch(const fdfb_ctx* c, const void* ksk, const uint
   return keyswitch_lwe(c, (const u64*)ksk, lwe_N, (int)B, lwe_n, workspace, S(stream));
 }
 
+extern "C" size_t fdfb_workspace_poly_mul(const fdfb_ctx* c, uint32_t count) {
+  return c ? align256((size_t)count * c->prm.N * 8) : 0;
+}
 extern "C" int fdfb_poly_mul(const fdfb_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
-                             void* stream) {
+                             void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
   if (!a || !b || !out) return FDFB_E_NULL;
+  if (!workspace) return FDFB_E_WORKSPACE;
   cudaStream_t st = S(stream);
   const int N = c->prm.N;
-  u64* tb;
-  CK(cudaMallocAsync(&tb, (size_t)count * N * 8, st));
+  u64* tb = (u64*)workspace;
   CK(cudaMemcpyAsync(out, a, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(tb, b, (size_t)count * N * 8, cudaMemcpyDeviceToDevice, st));
   int rc = launch_ntt_batch(c, out, count, 0, st);
@@ -1130,7 +1233,6 @@ extern "C" int fdfb_poly_mul(const fdfb_ctx* c, const uint64_t* a, const uint64_
     CKL(c);
     rc = launch_ntt_batch(c, out, count, 1, st);
   }
-  cudaFreeAsync(tb, st);
   return rc;
 }
 
@@ -1146,24 +1248,28 @@ extern "C" int fdfb_lwe_decrypt(const fdfb_ctx* c, const int8_t* sk, const uint6
   return FDFB_OK;
 }
 
+extern "C" size_t fdfb_workspace_rlwe_phase(const fdfb_ctx* c, uint32_t count) {
+  return c ? 3 * align256((size_t)count * c->prm.N * 8) + fdfb_workspace_poly_mul(c, count) : 0;
+}
 extern "C" int fdfb_rlwe_phase(const fdfb_ctx* c, const int8_t* sk, const uint64_t* ct, uint32_t count, uint64_t* out,
-                               void* stream) {
+                               void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
   if (!sk || !ct || !out) return FDFB_E_NULL;
+  if (!workspace) return FDFB_E_WORKSPACE;
   cudaStream_t st = S(stream);
   const size_t tot = (size_t)count * c->prm.N;
-  u64* buf;
-  CK(cudaMallocAsync(&buf, 3 * tot * 8, st));
-  u64 *a = buf, *sp = buf + tot, *prod = buf + 2 * tot;
+  u64* a = (u64*)workspace;
+  u64* sp = (u64*)((char*)a + align256(tot * 8));
+  u64* prod = (u64*)((char*)sp + align256(tot * 8));
+  void* pm_ws = (char*)prod + align256(tot * 8);
   k_rlwe_phase_prep<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct, sk, (int)count, a, sp);
   CKL(c);
-  int rc = fdfb_poly_mul(c, a, sp, prod, count, st);
+  int rc = fdfb_poly_mul(c, a, sp, prod, count, pm_ws, st);
   if (!rc) {
     k_rlwe_phase_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, ct, prod, (int)count, out);
     CKL(c);
   }
-  cudaFreeAsync(buf, st);
   return rc;
 }
 

@@ -457,8 +457,8 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
-                  mb[k] += (u64)x[v][k] * kb[k];      // x < 16p < 2^32, K < p < 2^28: < 2^60 each,
-                  ma[k] += (u64)x[v][k] * ka[k];      // 2 ell <= 8 terms < 2^63 (redc64's range)
+                  mb[k] += (u64)x[v][k] * kb[k];      // x < fwd_out_bound p, K < p: setup_rns checks that
+                  ma[k] += (u64)x[v][k] * ka[k];      // 2 ell terms + the Montgomery term fit redc64
                 }
               }
             }
@@ -471,7 +471,7 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
           xb ^= 1;
           // CRT, accumulated prime by prime (thread-private coefficients tid + T k):
           //   t_i = r_i (P/p_i)^{-1} mod p_i,  V = sum_i t_i P/p_i - round(sum_i t_i / p_i) P,
-          // exact because |V| < 3P/8 keeps sum t_i/p_i within 3/8 of an integer.  acc += V mod Q
+          // exact because setup_rns picks P with 256 |V| + 17 NP P <= 128 P (crt_rounding_exact).  acc += V mod Q
           // as acc += t_i (P/p_i mod Q) per prime (unreduced: < 7Q < 2^57), while the sum of
           // floor(16 t_i / p_i) (<= 45, error < 3/16) rides in bits 58..63 of the same word.
 #pragma unroll
@@ -682,4 +682,48 @@ k_brk_rns(DevParams p, RnsParams R, const u64* __restrict__ canon, size_t row0, 
     const u32 v = csub32(red16(x[0][k], pr2), pr);
     o[k] = csub32(shoup32(v, R.ninv[pi], R.ninvs[pi], pr), pr);
   }
+}
+
+// brK export (the inverse of k_brk_rns): per prime, the inverse NTT_p of the stored slots
+// gives y_i 2^32 row mod p_i (N^{-1} was folded in), times 2^{-32}: t_i = y_i row mod p_i; the
+// CRT  row = sum_i t_i (P / p_i) mod P  is exact because row < Q < P.  One CTA per (poly).
+struct BrkExportC {
+  u32 inv32[RNS_MAXP], inv32s[RNS_MAXP];   // 2^{-32} mod p_i and its Shoup companion
+  u64 Pi[RNS_MAXP];                        // P / p_i
+  u64 P_lo, P_hi;                          // P
+};
+template <int N>
+__global__ void __launch_bounds__(N / 8)
+k_brk_export(DevParams p, RnsParams R, BrkExportC X, const u32* __restrict__ dev, size_t row0, u64* __restrict__ canon) {
+  using S = BrShape<N>;
+  constexpr int T = S::T;
+  __shared__ u32 sb[Lay<N>::WORDS];
+  const int tid = threadIdx.x;
+  const size_t poly = blockIdx.x;
+  const size_t frow = row0 + poly / 2;
+  const int col = (int)(poly % 2);
+  const int rows_per_step = 2 * p.ell_rgsw;
+  const size_t step = frow / rows_per_step;
+  const int r = (int)(frow % rows_per_step);
+  unsigned __int128 acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) acc[k] = 0;
+  for (int pi = 0; pi < R.np; pi++) {
+    const u32 pr = R.p[pi], pr2 = R.p2[pi];
+    const u32* src = dev + ((step * R.np + pi) * rows_per_step + r) * 2 * (size_t)N + (size_t)col * N + 8 * tid;
+    u32 x[1][8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[0][k] = src[k];
+    __syncthreads();                                  // sb of the previous prime fully read
+    ntt_inv32<N, 1>(x, sb, tid, R.itab + (size_t)pi * S::GROUPS * 4, pr, pr2, R.zero);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const u32 t = csub32(shoup32(csub32(x[0][k], pr), X.inv32[pi], X.inv32s[pi], pr), pr);
+      acc[k] += (unsigned __int128)t * X.Pi[pi];
+    }
+  }
+  const unsigned __int128 P = ((unsigned __int128)X.P_hi << 64) | X.P_lo;
+  u64* o = canon + (2 * row0 + poly) * (size_t)N;
+#pragma unroll
+  for (int k = 0; k < 8; k++) o[tid + T * k] = (u64)(acc[k] % P);
 }

@@ -151,19 +151,21 @@ __global__ void k_rlwe_finish(DevParams p, int kind, const u64* __restrict__ idx
   }
 }
 // generic RLWE encryption of arbitrary message polynomials (domain 8, object c)
-__global__ void k_rlwe_enc_mask(DevParams p, u64 seed, int count, u64* __restrict__ outmask) {
+__global__ void k_rlwe_enc_mask(DevParams p, u64 seed, int count, u64 obj0, u64* __restrict__ outmask) {
   int e = blockIdx.y;
+  const u64 obj = obj0 + e;                          // global object index (sharded batches)
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.N; c += gridDim.x * blockDim.x) {
-    u64 hi = rnd_word(seed, 8, e, 0, 0, 2 * (u64)c), lo = rnd_word(seed, 8, e, 0, 0, 2 * (u64)c + 1);
+    u64 hi = rnd_word(seed, 8, obj, 0, 0, 2 * (u64)c), lo = rnd_word(seed, 8, obj, 0, 0, 2 * (u64)c + 1);
     outmask[(size_t)e * p.N + c] = uniform_mod_q(hi, lo, p.Q);
   }
 }
-__global__ void k_rlwe_enc_finish(DevParams p, u64 seed, int count, const u64* __restrict__ msg,
+__global__ void k_rlwe_enc_finish(DevParams p, u64 seed, int count, u64 obj0, const u64* __restrict__ msg,
                                   const u64* __restrict__ mask, const u64* __restrict__ prod, u64* __restrict__ out) {
   int e = blockIdx.y;
   const u64 Q = p.Q;
+  const u64 obj = obj0 + e;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.N; c += gridDim.x * blockDim.x) {
-    long long err = gauss_cdt(rnd_word(seed, 8, e, 0, 0, 2 * (u64)p.N + c), p);
+    long long err = gauss_cdt(rnd_word(seed, 8, obj, 0, 0, 2 * (u64)p.N + c), p);
     size_t o = (size_t)e * p.N + c;
     out[(size_t)e * 2 * p.N + c] = add_mod(add_mod(prod[o], msg[o] % Q, Q), from_signed(err, Q), Q);
     out[(size_t)e * 2 * p.N + p.N + c] = mask[o];
@@ -199,9 +201,10 @@ __global__ void k_ksk_gen(DevParams p, u64 seed, const int8_t* s_lwe, const int8
 }
 // input ciphertexts of m in Z_t (domain 7).  flags bit0: mod-switch-exact variant.
 __global__ void k_lwe_encrypt(DevParams p, u64 seed, const int8_t* s_lwe, const u64* __restrict__ msg, int count,
-                              u32 flags, u64* __restrict__ out) {
+                              u32 flags, u64 obj0, u64* __restrict__ out) {
   int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= count) return;
+  const u64 obj = obj0 + w;                          // global object index (sharded batches)
   const u64 delta = (1ULL << p.log_q_lwe) / p.t;
   u64* o = out + (size_t)w * (p.n + 1);
   if (flags & 1) {
@@ -209,7 +212,7 @@ __global__ void k_lwe_encrypt(DevParams p, u64 seed, const int8_t* s_lwe, const 
     const u64 step = 1ULL << (p.log_q_lwe - log2N);
     u64 acc = 0;
     for (int i = lane; i < p.n; i += 32) {
-      u64 ai = (rnd_word(seed, 7, w, 0, 0, i) >> (64 - log2N)) * step;
+      u64 ai = (rnd_word(seed, 7, obj, 0, 0, i) >> (64 - log2N)) * step;
       o[1 + i] = ai;
       acc += ai * (u64)(long long)s_lwe[i];
     }
@@ -217,7 +220,7 @@ __global__ void k_lwe_encrypt(DevParams p, u64 seed, const int8_t* s_lwe, const 
     for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
     if (lane == 0) o[0] = (acc + delta * msg[w]) & p.q_mask;
   } else {
-    lwe_encrypt_warp(p, seed, 7, w, 0, s_lwe, delta * msg[w], o, lane);
+    lwe_encrypt_warp(p, seed, 7, obj, 0, s_lwe, delta * msg[w], o, lane);
   }
 }
 

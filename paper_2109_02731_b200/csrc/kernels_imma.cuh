@@ -5,13 +5,18 @@
 //   D[r][c] = sum_k A[r][k] * B[c][k]          (int8 x int8 -> int32, exact)
 //
 // A (rows = digit limbs / 0-1 rows of the ciphertexts) and B (rows = balanced base-256
-// digits of the key coefficients) are both K-major in global memory.  Per CTA (one per
-// SM, persistent over the output tiles, 256 threads, warp-specialised):
+// digits of the key coefficients) are both K-major in global memory.  CG = 2 (default): a
+// CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with tcgen05.mma.cta_group::2,
+// each CTA holding its 128 rows of A and BN/2 rows of B per stage, so each SM streams half
+// the operand bytes of a 1-CTA 128 x BN tile per MMA (CG = 1 is kept for A/B runs).
+// Per CTA (one per SM, persistent over the output tiles, 256 threads, warp-specialised):
 //   warp 0      TMA producer: cp.async.bulk.tensor 2D loads of a 128 x 128 B tile of A and
-//               a BN x 128 B tile of B per stage (SWIZZLE_128B), STAGES-deep mbarrier ring;
-//   warp 1      MMA issuer (one thread): tcgen05.mma.cta_group::1.kind::i8, M = 128,
+//               a BN/CG x 128 B tile of B per stage (SWIZZLE_128B), STAGES-deep mbarrier ring
+//               (CG = 2: both CTAs' loads complete on the leader CTA's barrier);
+//   warp 1      MMA issuer (one thread of the leader CTA): tcgen05.mma.kind::i8, M = 128 CG,
 //               N = BN, K = 32 per instruction, accumulators (int32) in TMEM, two
 //               accumulator buffers so the epilogue of tile t overlaps the MMAs of t + 1;
+//               its commits arrive on both CTAs' barriers (multicast);
 //   warp 2      TMEM allocator (512 columns);
 //   warps 4..7  epilogue: tcgen05.ld of the accumulator rows (one TMEM lane = one row per
 //               thread) and the exact recombination of the digit planes, see below.
@@ -30,17 +35,19 @@
 #include "common.cuh"
 
 namespace imma {
-constexpr int BM = 128;                      // rows per tile (TMEM lanes)
+constexpr int BM = 128;                      // rows per CTA tile (TMEM lanes)
 constexpr int BK = 128;                      // K bytes per stage (one 128-byte swizzle atom)
 constexpr int WT = 32;                       // output words per tile
 constexpr int BN = 7 * WT;                   // 224 accumulator columns per tile
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK;             // 16 KB
-constexpr int B_BYTES = BN * BK;             // 28 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_COLS = 256;                // TMEM columns per accumulator buffer (2 buffers)
 constexpr int THREADS = 256;
-constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+template <int CG> struct Cfg {
+  static constexpr int STAGES = CG == 2 ? 7 : 4;
+  static constexpr int A_BYTES = BM * BK;                // 16 KB
+  static constexpr int B_BYTES = (BN / CG) * BK;         // 28 KB / 14 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // multiple of 1024 (SW128 atoms)
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
 }  // namespace imma
 
 // epilogue parameters
@@ -84,6 +91,46 @@ FDFB_DEV void tma_load_2d(const CUtensorMap* tm, void* dst, uint64_t* bar, int x
       "l"(tm), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+FDFB_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+FDFB_DEV uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {   // shared::cluster address in CTA `rank`
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+FDFB_DEV void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+FDFB_DEV void cluster_sync_all() {   // every thread of both CTAs (warps reconverged by the caller)
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+// CTA-pair TMA load: lands in this CTA's smem, completes on the barrier at cluster address bar_c
+FDFB_DEV void tma_load_2d_pair(const CUtensorMap* tm, void* dst, uint32_t bar_c, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(bar_c), "r"(x), "r"(y)
+      : "memory");
+}
+FDFB_DEV void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit of the pair's MMAs: arrive on the barrier at this smem offset in both CTAs
+FDFB_DEV void umma_commit_pair(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(b))
+      : "memory");
+}
 FDFB_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 FDFB_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // K-major, 128-byte-swizzled operand tile: rows of 128 B, 8-row groups 1024 B apart
@@ -121,10 +168,14 @@ FDFB_DEV void tmem_ld8(uint32_t taddr, int (&v)[8]) {
 FDFB_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- the kernel
+template <int CG>
 __global__ void __launch_bounds__(imma::THREADS, 1)
 k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int tiles_m,
        int tiles_n, DevParams dp, ImmaEpi e) {
   using namespace imma;
+  using C = Cfg<CG>;
+  constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int TM = BM * CG;                          // rows per (pair) tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // SW128 atoms: 1024-B aligned
   uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -135,46 +186,64 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = tiles_m * tiles_n;
   const int nk = (K + BK - 1) / BK;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;     // pair (or CTA) index
+  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int b = 0; b < 2; b++) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 128); }
+    for (int b = 0; b < 2; b++) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 128 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncwarp();
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    if (lane == 0) {                                   // ---- TMA producer
+    if (lane == 0) {                                   // ---- TMA producer (each CTA loads its own halves)
       int st = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = unit; tile < ntiles; tile += nunits) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int arow = tm * TM + (int)rank * BM, brow = tn * BN + (int)rank * (BN / CG);
         for (int kb = 0; kb < nk; kb++) {
           mbar_wait(empty + st, ph ^ 1);
           uint8_t* sa = smem + st * STAGE_BYTES;
-          mbar_expect_tx(full + st, STAGE_BYTES);
-          tma_load_2d(&tmA, sa, full + st, kb * BK, tm * BM);
-          tma_load_2d(&tmB, sa + A_BYTES, full + st, kb * BK, tn * BN);
+          if constexpr (CG == 2) {
+            const uint32_t fb = mapa_rank(smem_u32(full + st), 0);   // the leader's barrier
+            if (leader) mbar_expect_tx(full + st, 2 * STAGE_BYTES);
+            tma_load_2d_pair(&tmA, sa, fb, kb * BK, arow);
+            tma_load_2d_pair(&tmB, sa + A_BYTES, fb, kb * BK, brow);
+          } else {
+            mbar_expect_tx(full + st, STAGE_BYTES);
+            tma_load_2d(&tmA, sa, full + st, kb * BK, arow);
+            tma_load_2d(&tmB, sa + A_BYTES, full + st, kb * BK, brow);
+          }
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                   // ---- MMA issuer
-      constexpr uint32_t idesc = umma_idesc_i8(BM, BN);
+    if (lane == 0 && leader) {                         // ---- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_i8(TM, BN);
       int st = 0, ab = 0;
       uint32_t ph = 0, aph = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        mbar_wait(tempty + ab, aph ^ 1);              // epilogue drained this accumulator
+      for (int tile = unit; tile < ntiles; tile += nunits) {
+        mbar_wait(tempty + ab, aph ^ 1);              // epilogues drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(ab * ACC_COLS);
         for (int kb = 0; kb < nk; kb++) {
@@ -182,26 +251,31 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES), sb = sa + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 32; k++)
-            umma_i8(d, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), idesc, (kb | k) != 0);
-          umma_commit(empty + st);                     // smem slot free once these MMAs retire
+          for (int k = 0; k < BK / 32; k++) {
+            if constexpr (CG == 2)
+              umma_i8_pair(d, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), idesc, (kb | k) != 0);
+            else
+              umma_i8(d, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), idesc, (kb | k) != 0);
+          }
+          if constexpr (CG == 2) umma_commit_pair(empty + st); else umma_commit(empty + st);   // slots free
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
-        umma_commit(tfull + ab);                       // accumulator complete
+        if constexpr (CG == 2) umma_commit_pair(tfull + ab); else umma_commit(tfull + ab);     // accumulator complete
         if (++ab == 2) { ab = 0; aph ^= 1; }
       }
     }
   } else if (warp >= 4) {                              // ---- epilogue (lane quarter = warp % 4)
     const int q = warp & 3;
-    const int row_in_tile = q * 32 + lane;
+    const int row_in_tile = (int)rank * BM + q * 32 + lane;
+    const uint32_t tempty_c = CG == 2 ? mapa_rank(smem_u32(tempty), 0) : 0;   // the leader's tempty[0]
     int ab = 0;
     uint32_t aph = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int tile = unit; tile < ntiles; tile += nunits) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       mbar_wait(tfull + ab, aph);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * ACC_COLS);
-      const int row = tm * BM + row_in_tile;
+      const int row = tm * TM + row_in_tile;
       if (e.mode == 2) {                               // raw int32 accumulators
         int* o = (int*)e.out + (size_t)row * e.ldo;
 #pragma unroll 1
@@ -266,12 +340,18 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty + ab);
+      if constexpr (CG == 2) mbar_arrive_cluster(tempty_c + 8 * ab); else mbar_arrive(tempty + ab);
       if (++ab == 2) { ab = 0; aph ^= 1; }
     }
   }
+  __syncwarp();                                        // role loops ran on lane 0 only
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
 }

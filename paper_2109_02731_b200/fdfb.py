@@ -45,7 +45,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_workspace_keyswitch", "fdfb_workspace_bootstrap_multi", "fdfb_bootstrap_multi_batch",
             "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute",
             "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch", "fdfb_lwe_decrypt", "fdfb_rlwe_phase",
-            "fdfb_gemm_i8"]
+            "fdfb_gemm_i8", "fdfb_workspace_keygen", "fdfb_workspace_keygen_canonical",
+            "fdfb_workspace_rlwe_encrypt", "fdfb_workspace_poly_mul", "fdfb_workspace_rlwe_phase"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -73,11 +74,16 @@ def lib():
         L.fdfb_workspace_shift.restype = sz
         L.fdfb_workspace_vector_pack.argtypes = [vp, u32, u32]
         L.fdfb_workspace_vector_pack.restype = sz
-        L.fdfb_keygen.argtypes = [vp, u64, u32, vp, vp, vp, vp, vp, vp, vp]
-        L.fdfb_keygen_canonical.argtypes = [vp, u64, C.c_int, vp, vp, vp, u32, vp, vp]
+        L.fdfb_keygen.argtypes = [vp, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.fdfb_keygen_canonical.argtypes = [vp, u64, C.c_int, vp, vp, vp, u32, vp, vp, vp]
+        for f, a in (("fdfb_workspace_keygen", [vp]), ("fdfb_workspace_keygen_canonical", [vp, u32]),
+                     ("fdfb_workspace_rlwe_encrypt", [vp, u32]), ("fdfb_workspace_poly_mul", [vp, u32]),
+                     ("fdfb_workspace_rlwe_phase", [vp, u32])):
+            getattr(L, f).argtypes = a
+            getattr(L, f).restype = sz
         L.fdfb_key_import.argtypes = [vp, C.c_int, vp, vp, vp]
-        L.fdfb_lwe_encrypt.argtypes = [vp, u64, vp, vp, u32, u32, vp, vp]
-        L.fdfb_rlwe_encrypt.argtypes = [vp, u64, vp, vp, u32, vp, vp]
+        L.fdfb_lwe_encrypt.argtypes = [vp, u64, vp, vp, u32, u32, u64, vp, vp]
+        L.fdfb_rlwe_encrypt.argtypes = [vp, u64, vp, vp, u32, u64, vp, vp, vp]
         L.fdfb_setup_lut.argtypes = [vp, vp, u32, vp, vp]
         L.fdfb_bootstrap_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_bootstrap_batch_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
@@ -92,7 +98,7 @@ def lib():
         L.fdfb_workspace_bootstrap_shift.restype = sz
         L.fdfb_bootstrap_shift_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_lwe_decrypt.argtypes = [vp, vp, vp, u32, u32, vp, vp, vp]
-        L.fdfb_rlwe_phase.argtypes = [vp, vp, vp, u32, vp, vp]
+        L.fdfb_rlwe_phase.argtypes = [vp, vp, vp, u32, vp, vp, vp]
         L.fdfb_workspace_permute.argtypes = [vp, u32]
         L.fdfb_workspace_permute.restype = sz
         L.fdfb_permute.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
@@ -101,7 +107,7 @@ def lib():
         L.fdfb_vector_pack.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
         L.fdfb_shift.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_shift_streaming.argtypes = [vp, vp, vp, vp, vp, u32, vp]
-        L.fdfb_poly_mul.argtypes = [vp, vp, vp, vp, u32, vp]
+        L.fdfb_poly_mul.argtypes = [vp, vp, vp, vp, u32, vp, vp]
         L.fdfb_gemm_i8.argtypes = [vp, vp, vp, u32, u32, u32, vp, vp]
         L.fdfb_cdt_table.argtypes = [vp, vp, C.POINTER(C.c_int)]
         L.fdfb_launch_count.argtypes = [vp]
@@ -142,6 +148,17 @@ def _ptr(t):
 def _stream(stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+def _keep(stream, *tensors):
+    """Tensors allocated on the current stream but used by kernels enqueued on `stream`:
+    tell the caching allocator, so their memory is not handed out again before `stream`
+    has finished with it (temporaries dropped on return, outputs freed later)."""
+    if stream is None or stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            t.record_stream(stream)
 
 
 def params_from_config(cfg: dict, noiseless: bool = False) -> fdfb_params:
@@ -210,9 +227,11 @@ class Context:
         keys = {"s": sk[0], "S": sk[1]}
         for bit, name in ((2, "brk"), (4, "bpk"), (8, "ksk"), (16, "pack")):
             keys[name] = self._bytes(self.sizes[name]) if which & bit else None
+        ws = self._bytes(lib().fdfb_workspace_keygen(self.h)) if which & 30 else None
+        _keep(stream, ws, *[v for v in keys.values() if v is not None])
         _check(lib().fdfb_keygen(self.h, C.c_uint64(seed), which, _ptr(keys["s"]), _ptr(keys["S"]),
                                  _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]), _ptr(keys["pack"]),
-                                 _stream(stream)))
+                                 _ptr(ws), _stream(stream)))
         return keys
 
     def keygen_canonical(self, seed, kind, s, S, idx, stream=None):
@@ -220,27 +239,37 @@ class Context:
         idx = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64))
         per = (self.n + 1) if kind == KEY_KSK else 2 * self.N
         out = self._u64(len(idx), per)
+        ws = self._bytes(lib().fdfb_workspace_keygen_canonical(self.h, len(idx)))
+        _keep(stream, out, ws)
         _check(lib().fdfb_keygen_canonical(self.h, C.c_uint64(seed), kind, _ptr(s), _ptr(S),
-                                           idx.ctypes.data_as(C.c_void_p), len(idx), _ptr(out), _stream(stream)))
+                                           idx.ctypes.data_as(C.c_void_p), len(idx), _ptr(out), _ptr(ws),
+                                           _stream(stream)))
         return out
 
     def key_import(self, kind: int, canonical: torch.Tensor, stream=None):
         name = {KEY_BRK: "brk", KEY_BPK: "bpk", KEY_KSK: "ksk", KEY_PACK: "pack"}[kind]
         dev = self._bytes(self.sizes[name])
-        _check(lib().fdfb_key_import(self.h, kind, _ptr(canonical.contiguous()), _ptr(dev), _stream(stream)))
+        canonical = canonical.contiguous()
+        _keep(stream, dev, canonical)
+        _check(lib().fdfb_key_import(self.h, kind, _ptr(canonical), _ptr(dev), _stream(stream)))
         return dev
 
     def key_export(self, kind: int, dev_key: torch.Tensor, stream=None):
-        name = {KEY_BPK: "canon_bpk", KEY_KSK: "canon_ksk", KEY_PACK: "canon_pack"}[kind]
+        """Canonical (coefficient-domain) layout of a device key; BRK through inverse NTT + CRT."""
+        name = {KEY_BRK: "canon_brk", KEY_BPK: "canon_bpk", KEY_KSK: "canon_ksk", KEY_PACK: "canon_pack"}[kind]
         out = self._u64(self.sizes[name] // 8)
+        _keep(stream, out)
         _check(lib().fdfb_key_export(self.h, kind, _ptr(dev_key), _ptr(out), _stream(stream)))
         return out
 
     # ---------------------------------------------------------------- inputs / LUT
-    def lwe_encrypt(self, seed, s, msgs: torch.Tensor, exact=False, stream=None):
+    def lwe_encrypt(self, seed, s, msgs: torch.Tensor, exact=False, first_index=0, stream=None):
+        """LWE encryptions of msgs; ciphertext c is object first_index + c of the seed's stream
+        (a shard passes its global offset and gets exactly the single-device ciphertexts)."""
         out = self._u64(msgs.numel(), self.n + 1)
+        _keep(stream, out)
         _check(lib().fdfb_lwe_encrypt(self.h, C.c_uint64(seed), _ptr(s), _ptr(msgs), msgs.numel(),
-                                      1 if exact else 0, _ptr(out), _stream(stream)))
+                                      1 if exact else 0, C.c_uint64(first_index), _ptr(out), _stream(stream)))
         return out
 
     def lwe_decrypt(self, s, ct, t=None, stream=None):
@@ -249,6 +278,7 @@ class Context:
         B = ct.shape[0]
         phase = self._u64(B)
         msg = self._u64(B) if t else None
+        _keep(stream, phase, msg)
         _check(lib().fdfb_lwe_decrypt(self.h, _ptr(s), _ptr(ct), B, int(t or 0), _ptr(phase), _ptr(msg),
                                       _stream(stream)))
         return phase, msg
@@ -257,14 +287,18 @@ class Context:
         """b - a * S mod Q of every RLWE ciphertext [B, 2, N] (fdfb_rlwe_phase)."""
         B = ct.shape[0]
         out = self._u64(B, self.N)
-        _check(lib().fdfb_rlwe_phase(self.h, _ptr(S), _ptr(ct), B, _ptr(out), _stream(stream)))
+        ws = self._bytes(lib().fdfb_workspace_rlwe_phase(self.h, B))
+        _keep(stream, out, ws)
+        _check(lib().fdfb_rlwe_phase(self.h, _ptr(S), _ptr(ct), B, _ptr(out), _ptr(ws), _stream(stream)))
         return out
 
-    def rlwe_encrypt(self, seed, S, msgs: torch.Tensor, stream=None):
+    def rlwe_encrypt(self, seed, S, msgs: torch.Tensor, first_index=0, stream=None):
         cnt = msgs.shape[0]
         out = self._u64(cnt, 2, self.N)
-        _check(lib().fdfb_rlwe_encrypt(self.h, C.c_uint64(seed), _ptr(S), _ptr(msgs), cnt, _ptr(out),
-                                       _stream(stream)))
+        ws = self._bytes(lib().fdfb_workspace_rlwe_encrypt(self.h, cnt))
+        _keep(stream, out, ws)
+        _check(lib().fdfb_rlwe_encrypt(self.h, C.c_uint64(seed), _ptr(S), _ptr(msgs), cnt, C.c_uint64(first_index),
+                                       _ptr(out), _ptr(ws), _stream(stream)))
         return out
 
     def setup_lut(self, lut, t_out=None, stream=None):
@@ -272,6 +306,7 @@ class Context:
         lut = np.ascontiguousarray(np.asarray(lut, dtype=np.uint64))
         t_out = self.cfg["t"] if t_out is None else t_out
         rotp = self._u64(2, self.N)
+        _keep(stream, rotp)
         _check(lib().fdfb_setup_lut(self.h, lut.ctypes.data_as(C.c_void_p), t_out, _ptr(rotp), _stream(stream)))
         return rotp
 
@@ -283,6 +318,7 @@ class Context:
         B = ct_in.shape[0]
         ct_out = self._u64(B, self.n + 1) if ct_out is None else ct_out
         ws = self.workspace_bootstrap(B) if workspace is None else workspace
+        _keep(stream, ct_out, ws)
         _check(lib().fdfb_bootstrap_batch(self.h, _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]),
                                           _ptr(rotp), _ptr(ct_in), _ptr(ct_out), B, _ptr(ws), _stream(stream)))
         return ct_out
@@ -292,8 +328,10 @@ class Context:
         B, k = ct_in.shape[0], rotps.shape[0]
         out = self._u64(k, B, self.n + 1)
         ws = self._bytes(lib().fdfb_workspace_bootstrap_multi(self.h, B, k)) if workspace is None else workspace
+        rotps = rotps.contiguous()
+        _keep(stream, out, ws, rotps)
         _check(lib().fdfb_bootstrap_multi_batch(self.h, _ptr(keys["brk"]), _ptr(keys["bpk"]), _ptr(keys["ksk"]),
-                                                _ptr(rotps.contiguous()), k, _ptr(ct_in), _ptr(out), B, _ptr(ws),
+                                                _ptr(rotps), k, _ptr(ct_in), _ptr(out), B, _ptr(ws),
                                                 _stream(stream)))
         return out
 
@@ -302,6 +340,7 @@ class Context:
         B = ct_in.shape[0]
         out = self._u64(B, self.n + 1)
         ws = self.workspace_bootstrap(B) if workspace is None else workspace
+        _keep(stream, out, ws)
         _check(lib().fdfb_bootstrap_tfhe_batch(self.h, _ptr(keys["brk"]), _ptr(keys["ksk"]), _ptr(rotp), _ptr(ct_in),
                                                _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
@@ -314,6 +353,7 @@ class Context:
         B = ct_in.shape[0]
         out = self._u64(B, self.n + 1)
         ws = self.workspace_bootstrap_shift(B) if workspace is None else workspace
+        _keep(stream, out, ws)
         _check(lib().fdfb_bootstrap_shift_batch(self.h, _ptr(keys["brk"]), _ptr(pack), _ptr(keys["ksk"]), _ptr(rotp),
                                                 _ptr(ct_in), _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
@@ -333,6 +373,7 @@ class Context:
     def sample_extract(self, rlwe, k, stream=None):
         B = rlwe.shape[0]
         out = self._u64(B, self.N + 1)
+        _keep(stream, out)
         _check(lib().fdfb_sample_extract(self.h, _ptr(rlwe), _ptr(k), _ptr(out), B, _stream(stream)))
         return out
 
@@ -341,6 +382,7 @@ class Context:
         B = lwe.shape[0]
         out = self._u64(B, self.n + 1)
         ws = self._bytes(lib().fdfb_workspace_keyswitch(self.h, B)) if gemm else None
+        _keep(stream, out, ws)
         _check(lib().fdfb_lwe_keyswitch(self.h, _ptr(ksk), _ptr(lwe), _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
 
@@ -348,12 +390,14 @@ class Context:
         B, m = lwe.shape[0], lwe.shape[1]
         out = self._u64(B, 2, self.N)
         ws = self._bytes(lib().fdfb_workspace_vector_pack(self.h, m, B))
+        _keep(stream, out, ws)
         _check(lib().fdfb_vector_pack(self.h, _ptr(pack), _ptr(lwe), m, _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
 
     def pack(self, pack, lwe, d, stream=None):
         B = lwe.shape[0]
         out = self._u64(B, 2, self.N)
+        _keep(stream, out)
         _check(lib().fdfb_pack(self.h, _ptr(pack), _ptr(lwe), _ptr(d), _ptr(out), B, _stream(stream)))
         return out
 
@@ -368,6 +412,7 @@ class Context:
         B = rlwe.shape[0]
         out = self._u64(B, 2, self.N) if out is None else out
         ws = self.workspace_shift(B) if workspace is None else workspace
+        _keep(stream, out, ws)
         _check(lib().fdfb_shift(self.h, _ptr(pack), _ptr(rlwe), _ptr(d), _ptr(out), B, _ptr(ws), _stream(stream)))
         return out
 
@@ -377,6 +422,7 @@ class Context:
         out = self._u64(B, 2, self.N) if out is None else out
         n = lib().fdfb_workspace_permute(self.h, B)
         ws = self._bytes(n) if n else None
+        _keep(stream, out, ws)
         _check(lib().fdfb_permute(self.h, _ptr(pack), _ptr(rlwe), _ptr(perm), _ptr(out), B, _ptr(ws),
                                   _stream(stream)))
         return out
@@ -384,12 +430,15 @@ class Context:
     def shift_streaming(self, pack, rlwe, d, out=None, stream=None):
         B = rlwe.shape[0]
         out = self._u64(B, 2, self.N) if out is None else out
+        _keep(stream, out)
         _check(lib().fdfb_shift_streaming(self.h, _ptr(pack), _ptr(rlwe), _ptr(d), _ptr(out), B, _stream(stream)))
         return out
 
     def poly_mul(self, a, b, stream=None):
         out = torch.empty_like(a)
-        _check(lib().fdfb_poly_mul(self.h, _ptr(a), _ptr(b), _ptr(out), a.shape[0], _stream(stream)))
+        ws = self._bytes(lib().fdfb_workspace_poly_mul(self.h, a.shape[0]))
+        _keep(stream, out, ws)
+        _check(lib().fdfb_poly_mul(self.h, _ptr(a), _ptr(b), _ptr(out), a.shape[0], _ptr(ws), _stream(stream)))
         return out
 
     def gemm_i8(self, A, B, stream=None):
@@ -397,6 +446,7 @@ class Context:
         M, K = A.shape
         Nc = B.shape[0]
         D = torch.empty((M, Nc), dtype=torch.int32, device=self.device)
+        _keep(stream, D)
         _check(lib().fdfb_gemm_i8(self.h, _ptr(A), _ptr(B), M, Nc, K, _ptr(D), _stream(stream)))
         return D
 

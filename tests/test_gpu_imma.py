@@ -46,8 +46,9 @@ def test_gemm_i8_matches_integer_product(M, Nc, K):
 
 
 def test_gemm_i8_extremes_and_many_tiles():
-    """All -128 x -128 (the largest positive int32 sums), all -128 x 127, and a grid of
-    2 x 148+ tiles so the persistent CTAs run several tiles through both TMEM buffers."""
+    """All -128 x -128 (the largest positive int32 sums), all -128 x 127, a grid of 160 tiles, and
+    one of 6 x 74 + 1 tiles so every persistent CTA (pair) runs >= 6 tiles through both TMEM
+    accumulator buffers (each buffer's full/empty barriers through several phases)."""
     K = 2048
     for a, b in ((-128, -128), (-128, 127), (127, 127)):
         A = np.full((130, K), a, np.int8)
@@ -58,6 +59,12 @@ def test_gemm_i8_extremes_and_many_tiles():
     rng = np.random.default_rng(3)
     A = rng.integers(-128, 128, (128 * 20, 512), dtype=np.int8)
     B = rng.integers(-128, 128, (224 * 16, 512), dtype=np.int8)
+    D = ctx().gemm_i8(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV))
+    torch.cuda.synchronize()
+    assert np.array_equal(D.cpu().numpy().astype(np.int64), ref(A, B))
+    # >= 6 tiles per persistent CTA (pair): both TMEM accumulator buffers through several phases
+    A = rng.integers(-128, 128, (256, 1024), dtype=np.int8)
+    B = rng.integers(-128, 128, (224 * 6 * 74 + 13, 1024), dtype=np.int8)
     D = ctx().gemm_i8(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV))
     torch.cuda.synchronize()
     assert np.array_equal(D.cpu().numpy().astype(np.int64), ref(A, B))
