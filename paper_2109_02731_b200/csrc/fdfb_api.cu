@@ -38,6 +38,7 @@ struct fdfb_ctx {
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
   int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 batched only, 1 auto (default), 2 / 3 force clusters of NP / 2 NP
   int imma_cg = 2;           // FDFB_IMMA_CG: int8 GEMM tiles per CTA pair (2, default) or per CTA (1)
+  int imma_wide_k = 65536;   // FDFB_IMMA_WIDE_K: K from which pair tiles are 448 columns wide
 };
 
 // Bracket one launch of kernel class `cls` with events on its stream when timing is on.
@@ -319,15 +320,15 @@ static int make_tmap_i8(CUtensorMap* m, const void* base, size_t rows, size_t K,
 // D = A [M][K] (pitch lda) x B [Ncols][K]^T (pitch ldb), both int8 K-major, through the
 // epilogue e (kernels_imma.cuh); Ncols is a multiple of imma::BN except in raw mode.  CTA pairs
 // (cta_group::2, 256-row tiles) unless FDFB_IMMA_CG=1.
-template <int CG>
+template <int CG, int NSUB>
 static int imma_launch(const fdfb_ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, size_t M, size_t Ncols,
                        size_t K, const ImmaEpi& e, int kclass, cudaStream_t st) {
   const int tiles_m = (int)((M + imma::BM * CG - 1) / (imma::BM * CG));
-  const int tiles_n = (int)((Ncols + imma::BN - 1) / imma::BN);
+  const int tiles_n = (int)((Ncols + imma::BN * NSUB - 1) / (imma::BN * NSUB));
   const long long nt = (long long)tiles_m * tiles_n;
   const int units = (int)(nt < c->num_sms / CG ? nt : c->num_sms / CG);
-  const size_t smem = imma::Cfg<CG>::SMEM;
-  CK(cudaFuncSetAttribute(k_imma<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = imma::Cfg<CG, NSUB>::SMEM;
+  CK(cudaFuncSetAttribute(k_imma<CG, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
   cfg.blockDim = dim3(imma::THREADS);
@@ -339,7 +340,7 @@ static int imma_launch(const fdfb_ctx* c, const CUtensorMap& ta, const CUtensorM
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   TimedLaunch tl(c, kclass, st);
-  CK(cudaLaunchKernelEx(&cfg, k_imma<CG>, ta, tb, (int)K, tiles_m, tiles_n, c->dp, e));
+  CK(cudaLaunchKernelEx(&cfg, k_imma<CG, NSUB>, ta, tb, (int)K, tiles_m, tiles_n, c->dp, e));
   CKL(c);
   return FDFB_OK;
 }
@@ -351,8 +352,11 @@ static int imma_gemm(const fdfb_ctx* c, const int8_t* A, size_t M, size_t lda, c
   int rc = make_tmap_i8(&ta, A, M, K, lda, imma::BM);
   if (!rc) rc = make_tmap_i8(&tb, B, Ncols, K, ldb, imma::BN / cg);
   if (rc) return rc;
-  return cg == 2 ? imma_launch<2>(c, ta, tb, M, Ncols, K, e, kclass, st)
-                 : imma_launch<1>(c, ta, tb, M, Ncols, K, e, kclass, st);
+  // long K (the epilogue is negligible next to a tile's MMAs): 448-column tiles, one accumulator
+  const bool wide = cg == 2 && K >= (size_t)c->imma_wide_k && Ncols % (2 * imma::BN) == 0;
+  if (cg == 1) return imma_launch<1, 1>(c, ta, tb, M, Ncols, K, e, kclass, st);
+  return wide ? imma_launch<2, 2>(c, ta, tb, M, Ncols, K, e, kclass, st)
+              : imma_launch<2, 1>(c, ta, tb, M, Ncols, K, e, kclass, st);
 }
 
 // ------------------------------------------------------------------ key switching
@@ -625,6 +629,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   if ((rc = setup_rns(c))) { delete c; return rc; }
   if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
   if (const char* e = getenv("FDFB_IMMA_CG")) c->imma_cg = atoi(e) == 1 ? 1 : 2;
+  if (const char* e = getenv("FDFB_IMMA_WIDE_K")) c->imma_wide_k = atoi(e);
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));
   d.Q = Q; d.Q2 = 2 * Q; d.Q4 = 4 * Q; d.half = (Q + 1) / 2;

@@ -41,11 +41,16 @@ constexpr int WT = 32;                       // output words per tile
 constexpr int BN = 7 * WT;                   // 224 accumulator columns per tile
 constexpr int ACC_COLS = 256;                // TMEM columns per accumulator buffer (2 buffers)
 constexpr int THREADS = 256;
-template <int CG> struct Cfg {
-  static constexpr int STAGES = CG == 2 ? 7 : 4;
-  static constexpr int A_BYTES = BM * BK;                // 16 KB
-  static constexpr int B_BYTES = (BN / CG) * BK;         // 28 KB / 14 KB
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // multiple of 1024 (SW128 atoms)
+// NSUB = 2 (long K): a tile is two N = BN MMAs per k-step (448 accumulator columns, one
+// accumulator buffer), so each SM streams 27 % fewer operand bytes per MMA; NSUB = 1: one MMA,
+// two accumulator buffers (epilogue of tile t overlaps the MMAs of tile t + 1).
+template <int CG, int NSUB = 1> struct Cfg {
+  static constexpr int NBUF = NSUB == 1 ? 2 : 1;                 // accumulator buffers
+  static constexpr int A_BYTES = BM * BK;                        // 16 KB
+  static constexpr int BSUB_BYTES = (BN / CG) * BK;              // 28 KB / 14 KB per sub-tile
+  static constexpr int STAGE_BYTES = A_BYTES + NSUB * BSUB_BYTES;  // multiple of 1024 (SW128 atoms)
+  static constexpr int STAGES = (int)((227 * 1024 - 1024 - 256) / STAGE_BYTES) > 8 ? 8
+                              : (int)((227 * 1024 - 1024 - 256) / STAGE_BYTES);
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 }  // namespace imma
@@ -168,21 +173,24 @@ FDFB_DEV void tmem_ld8(uint32_t taddr, int (&v)[8]) {
 FDFB_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- the kernel
-template <int CG>
+template <int CG, int NSUB>
 __global__ void __launch_bounds__(imma::THREADS, 1)
 k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int tiles_m,
        int tiles_n, DevParams dp, ImmaEpi e) {
   using namespace imma;
-  using C = Cfg<CG>;
-  constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  using C = Cfg<CG, NSUB>;
+  constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES, NBUF = C::NBUF;
+  constexpr int BSUB = C::BSUB_BYTES;
   constexpr int TM = BM * CG;                          // rows per (pair) tile
+  constexpr int TN = BN * NSUB;                        // accumulator columns per tile
+  constexpr int TW = WT * NSUB;                        // output words per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // SW128 atoms: 1024-B aligned
   uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = (uint32_t*)(tempty + 2);
+  uint64_t* tempty = tfull + NBUF;
+  uint32_t* tslot = (uint32_t*)(tempty + NBUF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = tiles_m * tiles_n;
   const int nk = (K + BK - 1) / BK;
@@ -195,7 +203,7 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int b = 0; b < 2; b++) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 128 * CG); }
+    for (int b = 0; b < NBUF; b++) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 128 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -219,7 +227,7 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       uint32_t ph = 0;
       for (int tile = unit; tile < ntiles; tile += nunits) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
-        const int arow = tm * TM + (int)rank * BM, brow = tn * BN + (int)rank * (BN / CG);
+        const int arow = tm * TM + (int)rank * BM, brow = tn * TN + (int)rank * (BN / CG);
         for (int kb = 0; kb < nk; kb++) {
           mbar_wait(empty + st, ph ^ 1);
           uint8_t* sa = smem + st * STAGE_BYTES;
@@ -227,11 +235,13 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const uint32_t fb = mapa_rank(smem_u32(full + st), 0);   // the leader's barrier
             if (leader) mbar_expect_tx(full + st, 2 * STAGE_BYTES);
             tma_load_2d_pair(&tmA, sa, fb, kb * BK, arow);
-            tma_load_2d_pair(&tmB, sa + A_BYTES, fb, kb * BK, brow);
+#pragma unroll
+            for (int j = 0; j < NSUB; j++) tma_load_2d_pair(&tmB, sa + A_BYTES + j * BSUB, fb, kb * BK, brow + j * BN);
           } else {
             mbar_expect_tx(full + st, STAGE_BYTES);
             tma_load_2d(&tmA, sa, full + st, kb * BK, arow);
-            tma_load_2d(&tmB, sa + A_BYTES, full + st, kb * BK, brow);
+#pragma unroll
+            for (int j = 0; j < NSUB; j++) tma_load_2d(&tmB, sa + A_BYTES + j * BSUB, full + st, kb * BK, brow + j * BN);
           }
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
@@ -239,7 +249,7 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {                         // ---- MMA issuer
-      constexpr uint32_t idesc = umma_idesc_i8(TM, BN);
+      constexpr uint32_t idesc = umma_idesc_i8(TM, BN);   // per MMA: M = 128 CG, N = 224
       int st = 0, ab = 0;
       uint32_t ph = 0, aph = 0;
       for (int tile = unit; tile < ntiles; tile += nunits) {
@@ -252,16 +262,20 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES), sb = sa + A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 32; k++) {
-            if constexpr (CG == 2)
-              umma_i8_pair(d, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), idesc, (kb | k) != 0);
-            else
-              umma_i8(d, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), idesc, (kb | k) != 0);
+#pragma unroll
+            for (int j = 0; j < NSUB; j++) {
+              const uint64_t ad = umma_desc_sw128(sa + 32 * k), bd = umma_desc_sw128(sb + j * BSUB + 32 * k);
+              if constexpr (CG == 2)
+                umma_i8_pair(d + j * BN, ad, bd, idesc, (kb | k) != 0);
+              else
+                umma_i8(d + j * BN, ad, bd, idesc, (kb | k) != 0);
+            }
           }
           if constexpr (CG == 2) umma_commit_pair(empty + st); else umma_commit(empty + st);   // slots free
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
         if constexpr (CG == 2) umma_commit_pair(tfull + ab); else umma_commit(tfull + ab);     // accumulator complete
-        if (++ab == 2) { ab = 0; aph ^= 1; }
+        if (++ab == NBUF) { ab = 0; aph ^= 1; }
       }
     }
   } else if (warp >= 4) {                              // ---- epilogue (lane quarter = warp % 4)
@@ -279,11 +293,11 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       if (e.mode == 2) {                               // raw int32 accumulators
         int* o = (int*)e.out + (size_t)row * e.ldo;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 8) {
+        for (int c = 0; c < TN; c += 8) {
           int v[8];
           tmem_ld8(tbase + c, v);
           tmem_ld_wait();
-          const int col = tn * BN + c;
+          const int col = tn * TN + c;
           if (row < e.rows) {
 #pragma unroll
             for (int i = 0; i < 8; i++)
@@ -297,10 +311,11 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         u64* o = (u64*)e.out + (size_t)g * e.ldo;
         const bool wrap = e.mode == 1;
 #pragma unroll 1
-        for (int c8 = 0; c8 < WT; c8 += 8) {
+        for (int c8 = 0; c8 < TW; c8 += 8) {
+          const int sub = c8 / WT, cw = c8 % WT;         // sub-tile (its own 7 digit planes), word
           int v[7][8];
 #pragma unroll
-          for (int l = 0; l < 7; l++) tmem_ld8(tbase + l * WT + c8, v[l]);
+          for (int l = 0; l < 7; l++) tmem_ld8(tbase + sub * BN + l * WT + cw, v[l]);
           tmem_ld_wait();
           u64 val[8];
 #pragma unroll
@@ -321,7 +336,7 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             }
             val[i] = acc;
           }
-          const int w0 = tn * WT + c8;
+          const int w0 = tn * TW + c8;
           if (row < e.rows) {
 #pragma unroll
             for (int i = 0; i < 8; i++) {
@@ -341,7 +356,7 @@ k_imma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       }
       tc_fence_before();
       if constexpr (CG == 2) mbar_arrive_cluster(tempty_c + 8 * ab); else mbar_arrive(tempty + ab);
-      if (++ab == 2) { ab = 0; aph ^= 1; }
+      if (++ab == NBUF) { ab = 0; aph ^= 1; }
     }
   }
   __syncwarp();                                        // role loops ran on lane 0 only

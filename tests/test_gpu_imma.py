@@ -68,3 +68,17 @@ def test_gemm_i8_extremes_and_many_tiles():
     D = ctx().gemm_i8(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV))
     torch.cuda.synchronize()
     assert np.array_equal(D.cpu().numpy().astype(np.int64), ref(A, B))
+
+
+@pytest.mark.parametrize("M,Nc,K", [(300, 448 * 3, 1040), (257, 448 * 160, 512)])
+def test_gemm_i8_wide_tiles(M, Nc, K, monkeypatch):
+    """The 448-column pair tiles (two N = 224 MMAs per k-step, one accumulator) that long-K
+    contractions (Shift, Permute) use, forced at small K; 160 tiles -> several per pair."""
+    monkeypatch.setenv("FDFB_IMMA_WIDE_K", "256")
+    c = Context(synth.load_config("tiny"), 0)
+    rng = np.random.default_rng(M + Nc + K)
+    A = rng.integers(-128, 128, (M, K), dtype=np.int8)
+    B = rng.integers(-128, 128, (Nc, K), dtype=np.int8)
+    D = c.gemm_i8(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV))
+    torch.cuda.synchronize()
+    assert np.array_equal(D.cpu().numpy().astype(np.int64), ref(A, B))
