@@ -45,19 +45,35 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        cmd = [NVCC] + FLAGS + ["-o", OUT, SRC]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log = os.path.join(HERE, "build.log")
-        with open(log, "w") as f:
-            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stderr[-6000:])
-            raise RuntimeError("nvcc failed (see %s)" % log)
-        with open(HASH, "w") as f:
-            f.write(source_hash())
-        if verbose:
-            sys.stderr.write(r.stderr)
+    """Compile libfdfb.so if stale.  Concurrent callers (torchrun ranks) serialise on a file
+    lock; nvcc writes a temporary file that replaces the library atomically, so no process
+    ever maps a half-written .so, and a process that waited finds it fresh and skips."""
+    import fcntl
+    if not (force or needs_build()):
+        return OUT
+    with open(OUT + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if force or needs_build():
+                tmp = "%s.tmp.%d" % (OUT, os.getpid())
+                cmd = [NVCC] + FLAGS + ["-o", tmp, SRC]
+                r = subprocess.run(cmd, capture_output=True, text=True)
+                log = os.path.join(HERE, "build.log")
+                with open(log, "w") as f:
+                    f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+                if r.returncode != 0:
+                    if os.path.exists(tmp):
+                        os.remove(tmp)
+                    sys.stderr.write(r.stderr[-6000:])
+                    raise RuntimeError("nvcc failed (see %s)" % log)
+                os.replace(tmp, OUT)
+                with open(HASH + ".tmp", "w") as f:
+                    f.write(source_hash())
+                os.replace(HASH + ".tmp", HASH)
+                if verbose:
+                    sys.stderr.write(r.stderr)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
     return OUT
 
 

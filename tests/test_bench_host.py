@@ -55,3 +55,16 @@ def test_reference_arm_prints_the_contract_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_reference_arm_config_matches_gpu_arm_and_times_its_sample():
+    """Both arms print the same config dict (bootstrap_config), and the reference arm's
+    ms_per_step is the measured duration of its (bounded) sample step, not a projection."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "3", "--cpu-seconds", "2"], capture_output=True, text=True, timeout=280,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["config"] == bench.bootstrap_config(synth.load_config("large"), 4096, 1)
+    assert 0.5 < line["ms_per_step"] / 1000.0 < 60.0
+    assert line["steps"] == 2
