@@ -38,6 +38,7 @@ struct fdfb_ctx {
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
   int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 batched only, 1 auto (default), 2 / 3 force clusters of NP / 2 NP
   int imma_cg = 2;           // FDFB_IMMA_CG: int8 GEMM tiles per CTA pair (2, default) or per CTA (1)
+  int br_kernel = 2;         // FDFB_BR_KERNEL: 2 pipelined k_blind_rotate_p (default), 1 k_blind_rotate
   int imma_wide_k = 65536;   // FDFB_IMMA_WIDE_K: K from which pair tiles are 448 columns wide
 };
 
@@ -225,6 +226,37 @@ template <int N, int NP, bool GIN>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
                        const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
   constexpr int T = N / 8;
+  if (c->br_kernel != 1) {                     // pipelined kernel (mbarrier-decoupled exchanges, d in TMEM)
+    const size_t sm = 43 * (size_t)N;          // acc 16N + X0/X1 18N + slabs 9N
+    cudaFuncSetAttribute(k_blind_rotate_p<N, NP, GIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_blind_rotate_p<N, NP, GIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blind_rotate_p<N, NP, GIN>, T, sm);
+    // the occupancy query under-reports this kernel (1 per SM at N = 2048 where registers and shared
+    // memory both allow 2, as ncu's launch__occupancy_limit_* confirm): also bound it directly
+    {
+      int smem_sm = 0, regs_sm = 0;
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
+      cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, c->device);
+      int by_smem = smem_sm / (int)(sm + 1024 + 64), by_regs = regs_sm / (T * 128);
+      int est = by_smem < by_regs ? by_smem : by_regs;
+      if (est > BrShape<N>::MINB) est = BrShape<N>::MINB;
+      if (est > per_sm) per_sm = est;
+    }
+    cudaGetLastError();
+    if (getenv("FDFB_DEBUG")) fprintf(stderr, "k_blind_rotate_p<%d,%d,%d>: %d CTAs per SM\n", N, NP, (int)GIN, per_sm);
+    if (per_sm < 1) per_sm = 1;
+    const int tmem_cap = 512 / (T > 128 ? 64 : 32);             // TMEM columns per CTA (d)
+    if (per_sm > tmem_cap) per_sm = tmem_cap;
+    int grid = c->num_sms * per_sm;
+    if (grid > n_acc) grid = n_acc;
+    TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
+    k_blind_rotate_p<N, NP, GIN><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar,
+                                                       gin, s_begin);
+    CKL(c);
+    return FDFB_OK;
+  }
   const size_t sm = 50 * (size_t)N;            // sacc 16N + sd 16N + 2 exchange buffers x 2 planes 9N bytes
   // function attributes are per device: set on every launch (host-side, ~µs), not once per process
   cudaFuncSetAttribute(k_blind_rotate<N, NP, GIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -629,6 +661,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   if ((rc = setup_rns(c))) { delete c; return rc; }
   if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
   if (const char* e = getenv("FDFB_IMMA_CG")) c->imma_cg = atoi(e) == 1 ? 1 : 2;
+  if (const char* e = getenv("FDFB_BR_KERNEL")) c->br_kernel = atoi(e) == 1 ? 1 : 2;
   if (const char* e = getenv("FDFB_IMMA_WIDE_K")) c->imma_wide_k = atoi(e);
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));

@@ -32,6 +32,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include "kernels_core.cuh"
+#include "kernels_imma.cuh"   // mbarrier / TMEM helpers
 
 #define RNS_MAXP 3
 
@@ -273,9 +274,9 @@ constexpr int fwd_bound_before_last() {
     return BOUND;
   }
 }
-template <int N, int q, int V>
+template <int N, int q, int V, int QMIN = 1>     // inverse passes q .. QMIN, stores layout QMIN - 1 last
 FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
-  if constexpr (q >= 1) {
+  if constexpr (q >= QMIN && q >= 1) {
     constexpr int T1 = N >> (3 * q + 3);
     const int B = qbase<N, q>(tid);
     xload<N, q, V>(x, sb, lay_base<N, q>(B), T1);
@@ -283,7 +284,7 @@ FDFB_DEV void inv_mid(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p,
     __syncwarp();
     xstore<N, q - 1, V>(x, sb, lay_base<N, q - 1>(B), T1);
     __syncwarp();
-    inv_mid<N, q - 1, V>(x, sb, tid, tab, p, p2, z);
+    inv_mid<N, q - 1, V, QMIN>(x, sb, tid, tab, p, p2, z);
   }
 }
 
@@ -296,12 +297,20 @@ FDFB_DEV void ntt_fwd32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 
   constexpr int T = S::T, NM = S::NMID;
   fwd8_32<V>(x, tab, p, p2, z);                       // inputs < 2p (digits < L <= p): bound 2 + 6
   xstore<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
+#ifdef FDFB_EXP_NOBAR
+  __syncwarp();
+#else
   __syncthreads();
+#endif
   fwd_mid<N, 1, V, 8>(x, sb, tid, tab, p, p2, z);
   xload<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
   constexpr int BL = fwd_bound_before_last<N, 1, 8>();
   if constexpr (BL + 2 * S::PLAST > 16) red8p_all<V>(x, p2);
+#ifdef FDFB_EXP_TW   // timing experiment only (wrong results): every thread reads one final-pass group
+  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + (tid & FDFB_EXP_TW)), p, p2, z);
+#else
   fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+#endif
 }
 // bound (in p) of the forward transform's outputs
 template <int N>
@@ -316,11 +325,19 @@ template <int N, int V>
 FDFB_DEV void ntt_inv32(u32 (&x)[V][8], u32* sb, int tid, const uint4* tab, u32 p, u32 p2, u32 z) {
   using S = BrShape<N>;
   constexpr int T = S::T, NM = S::NMID;
+#ifdef FDFB_EXP_TW
+  inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + (tid & FDFB_EXP_TW)), p, p2, z);
+#else
   inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+#endif
   xstore<N, NM - 1, V>(x, sb, lay_base<N, NM - 1>(8 * tid), 1);
   __syncwarp();
   inv_mid<N, NM - 1, V>(x, sb, tid, tab, p, p2, z);
+#ifdef FDFB_EXP_NOBAR
+  __syncwarp();
+#else
   __syncthreads();
+#endif
   xload<N, 0, V>(x, sb, lay_base<N, 0>(tid), T);
   inv8_32<V>(x, tab, p, p2, z);
 }
@@ -384,7 +401,11 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
       for (int j = j0; j < j1; j++) {
         // exponent -abar_i u_j mod 2N; u = [1] (binary) or [-1, 1] (ternary)
         const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
+#ifdef FDFB_EXP_KEY  // timing experiment only (wrong results): every step reads step 0's key
+        const u32* Kstep = bsk + 8 * tid;
+#else
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
+#endif
         int xb = 0;                                // exchange buffer of the next transform
         __syncthreads();                           // acc of the previous step complete
         // d = acc X^e - acc for both halves, once per CMux (thread-private slots of sd; the
@@ -403,10 +424,14 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
             for (int k = 0; k < 8; k++) {
               const int pos = tid + T * k;
+#ifdef FDFB_EXP_NOD
+              sd[half * N + pos] = src[pos] + e;
+#else
               const int idx = (pos - e) & (2 * N - 1);     // coefficient pos of X^e a = +-a[idx mod N]
               const u64 v = src[idx & (N - 1)];
               const u64 rv = (idx >= N && v) ? Q - v : v;
               sd[half * N + pos] = sub_mod(rv, src[pos], Q);
+#endif
             }
           }
         }
@@ -489,10 +514,12 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
                 const u32 kk = ((u32)(a >> 58) + f + 8) >> 4;                       // round(sum t_i / p_i)
                 a &= (1ull << 58) - 1;
                 a += (u64)(NP + 1) * Q - (u64)kk * R.pq;                            // kk <= NP, pq < Q
+#ifndef FDFB_EXP_NOCSUB
                 a = csub(a, Q << 3);
                 a = csub(a, Q << 2);
                 a = csub(a, Q << 1);
                 a = csub(a, Q);
+#endif
               }
               sa[pos] = a;
             }
@@ -504,6 +531,285 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 #pragma unroll
     for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
   }
+}
+
+// ---------------------------------------------------------------------------
+// k_blind_rotate_p: the batched kernel with the per-transform CTA barrier removed (the
+// default; k_blind_rotate above is kept for A/B, FDFB_BR_KERNEL=1).  Same arithmetic, same
+// output bytes.  Every transform has exactly one cross-warp exchange (after the forward
+// transform's first radix-8 pass, before the inverse transform's last one); here it goes
+// through one of two buffers X0/X1 guarded by mbarriers instead of __syncthreads:
+//   produce(c): ... -> wait empty[b] -> store the cross-warp layout into X[b] -> arrive full[b]
+//   consume(c): wait full[b] -> load from X[b] -> arrive empty[b] -> warp-local passes (own slab)
+// (b = c mod 2) and the schedule produces transform c + 1 before consuming transform c, so a
+// warp waits on the others only if they lag by more than a whole transform.  The warp-local
+// exchanges use a separate buffer (each warp touches only its own slab), so X[b] is released
+// as soon as it is loaded.  d = acc X^e - acc is thread-private and lives in TMEM (64 columns
+// per CTA: warps w and w + 4 share TMEM lanes and use column groups 0 / 32), which frees the
+// shared memory for the second buffer: 16N (acc) + 18N (X0, X1) + 9N (slabs) = 43N bytes
+// (86 KB at N = 2048; 2 CTAs per SM as before).  Per CMux:
+//   P(F0) P(F1) C(F0) P(F2) C(F1) P(F3) C(F2) C(F3) P(I) P(F0') C(I) P(F1') C(F0') ...
+// (F: forward digit-pair transforms of a prime, I: its inverse; ' = next prime).
+// one arrival per warp: __syncwarp orders the lanes' shared-memory accesses before lane 0's
+// (release) arrive, so the barriers count warps, not threads
+FDFB_DEV void warp_arrive(uint64_t* b) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(b);
+}
+template <int N, int V>
+FDFB_DEV void fwd_consume(u32 (&x)[V][8], const u32* X, u32* sl, int tid, const uint4* tab, u32 p, u32 p2, u32 z,
+                          uint64_t* empty_b) {
+  using S = BrShape<N>;
+  constexpr int T1 = N >> 6;                       // pass-1 stride
+  const int B = qbase<N, 1>(tid);
+  xload<N, 0, V>(x, X, lay_base<N, 0>(B), T1);
+  warp_arrive(empty_b);                            // this warp is done with X[b]
+  fwd8_32<V>(x, tab + 4 * (S::grp(1) + tid / T1), p, p2, z);   // inputs < 8p: no reduction
+  __syncwarp();                                    // laggard lanes done reading the slab
+  xstore<N, 1, V>(x, sl, lay_base<N, 1>(B), T1);
+  __syncwarp();
+  fwd_mid<N, 2, V, 14>(x, sl, tid, tab, p, p2, z);
+  xload<N, S::NMID - 1, V>(x, sl, lay_base<N, S::NMID - 1>(8 * tid), 1);
+  constexpr int BL = fwd_bound_before_last<N, 1, 8>();
+  if constexpr (BL + 2 * S::PLAST > 16) red8p_all<V>(x, p2);
+#ifdef FDFB_EXP_TW
+  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + (tid & FDFB_EXP_TW)), p, p2, z);
+#else
+  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+#endif
+}
+// inverse up to the cross-warp store: last pass in registers, warp-local passes through the
+// slab, pass 1 -> layout 0 into X[b]
+template <int N, int V>
+FDFB_DEV void inv_produce(u32 (&x)[V][8], u32* X, u32* sl, int tid, const uint4* tab, u32 p, u32 p2, u32 z,
+                          uint64_t* empty_b, uint32_t empty_par, uint64_t* full_b) {
+  using S = BrShape<N>;
+  constexpr int NM = S::NMID;
+  inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+  __syncwarp();
+  xstore<N, NM - 1, V>(x, sl, lay_base<N, NM - 1>(8 * tid), 1);
+  __syncwarp();
+  inv_mid<N, NM - 1, V, 2>(x, sl, tid, tab, p, p2, z);     // passes NM-1 .. 2 (slab), layout 1 stored
+  constexpr int T1 = N >> 6;
+  const int B = qbase<N, 1>(tid);
+  xload<N, 1, V>(x, sl, lay_base<N, 1>(B), T1);
+  inv8_32<V>(x, tab + 4 * (S::grp(1) + tid / T1), p, p2, z);
+  mbar_wait(empty_b, empty_par);
+  xstore<N, 0, V>(x, X, lay_base<N, 0>(B), T1);
+  warp_arrive(full_b);
+}
+
+template <int N, int NP, bool GIN>
+__global__ void __launch_bounds__(N / 8, BrShape<N>::MINB)
+k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
+                 int acc_per_ct, int abar_rows, const u32* __restrict__ abar, const u64* __restrict__ gin,
+                 int s_begin) {
+  using S = BrShape<N>;
+  constexpr int T = S::T;
+  constexpr int W = Lay<N>::WORDS;
+  static_assert(fwd_out_bound<N>() <= 16, "forward outputs must stay below 16p < 2^32 (MAC bound)");
+  extern __shared__ u64 smem[];
+  u64* sacc = smem;                                // [b | a], natural order, canonical mod Q
+  u32* Xb = (u32*)(smem + 2 * N);                  // X0, X1: 2 planes of W words each
+  u32* sl = Xb + 2 * 2 * W;                        // warp-local exchange slabs (2 planes of W words)
+  __shared__ uint64_t bars[4];                     // full[0..1], empty[2..3]
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const u64 Q = p.Q;
+  const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
+  const u32 dmask = (1u << logL) - 1;
+  const int PPH = (ell + 1) / 2;                   // digit pairs per half
+  const int NF = 2 * PPH;                          // forward transforms per prime
+  const size_t prime_words = (size_t)2 * ell * 2 * N;
+  const size_t step_words = (size_t)NP * prime_words;
+  if (tid == 0) {
+    for (int b = 0; b < 4; b++) mbar_init(bars + b, T / 32);   // one arrival per warp
+  }
+  constexpr int TCOLS = T > 128 ? 64 : 32;         // 32 words per thread; warps w, w + 4 share lanes
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // this thread's 32 TMEM words: lanes 32 (warp % 4) .., column group warp / 4
+  const uint32_t tm = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+  int cp = 0, cc = 0;                              // produced / consumed transform counters (uniform)
+  u32 x[2][8];
+  u64 mb[8], ma[8];
+
+  for (int g = blockIdx.x; g < n_acc; g += gridDim.x) {
+    u64* acc = accs + (size_t)g * 2 * N;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; k++) sacc[tid + T * k] = acc[tid + T * k];
+    const u32* ab = abar + (size_t)((g / acc_per_ct) % abar_rows) * p.n;
+    const int i0 = GIN ? s_begin / u : 0, i1 = GIN ? i0 + 1 : p.n;
+    const int j0 = GIN ? s_begin - i0 * u : 0, j1 = GIN ? j0 + 1 : u;
+#pragma unroll 1
+    for (int i = i0; i < i1; i++) {
+      const u32 ai = __ldg(ab + i);
+      if constexpr (GIN) {
+        if (ai == 0) continue;                     // Shift(acc, 0) = acc: CMux(brK, acc, acc) = acc
+      }
+#pragma unroll 1
+      for (int j = j0; j < j1; j++) {
+        const int e = (u == 2 && j == 0) ? (int)ai : (int)((2 * N - ai) & (2 * N - 1));
+#ifdef FDFB_EXP_KEY
+        const u32* Kstep = bsk + 8 * tid;
+#else
+        const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
+#endif
+        __syncthreads();                           // acc of the previous step complete
+        {                                          // d = acc X^e - acc (both halves) -> TMEM
+          u32 dw[16];
+#pragma unroll
+          for (int half = 0; half < 2; half++) {
+            const u64* src = sacc + half * N;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              const int pos = tid + T * k;
+              u64 dv;
+              if constexpr (GIN) {
+                dv = sub_mod(__ldg(gin + (size_t)g * 2 * N + half * N + pos), src[pos], Q);
+              } else {
+                const int idx = (pos - e) & (2 * N - 1);   // coefficient pos of X^e a = +-a[idx mod N]
+                const u64 v = src[idx & (N - 1)];
+                const u64 rv = (idx >= N && v) ? Q - v : v;
+                dv = sub_mod(rv, src[pos], Q);
+              }
+              dw[2 * k] = (u32)dv;
+              dw[2 * k + 1] = (u32)(dv >> 32);
+            }
+            tmem_st16(tm + 16 * half, dw);
+          }
+          tmem_st_wait();
+        }
+        // ---- the transform pipeline over the NP primes
+        auto produce_fwd = [&](int pi, int f) {
+          const int half = f >= PPH ? 1 : 0, r = 2 * (f - half * PPH);   // f < 2 PPH: no division
+          const bool two = r + 1 < ell;
+          u32 dw[16];
+          tmem_ld16(tm + 16 * half, dw);
+          tmem_ld_wait();
+          const int sh = r * logL;
+#pragma unroll
+          for (int k = 0; k < 8; k++) {
+            const u64 dv = ((u64)dw[2 * k + 1] << 32) | dw[2 * k];
+            x[0][k] = (u32)(dv >> sh) & dmask;
+            x[1][k] = two ? (u32)(dv >> (sh + logL)) & dmask : 0u;
+          }
+          const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
+          fwd8_32<2>(x, ft, R.p[pi], R.p2[pi], R.zero);          // pass 0 (inputs < 2p)
+          const int b = cp & 1;
+          mbar_wait(bars + 2 + b, ((cp >> 1) & 1) ^ 1);
+          xstore<N, 0, 2>(x, Xb + b * 2 * W, lay_base<N, 0>(tid), T);
+          warp_arrive(bars + b);
+          cp++;
+        };
+        auto consume_fwd = [&](int pi, int f) {
+          const int half = f >= PPH ? 1 : 0, r = 2 * (f - half * PPH);   // f < 2 PPH: no division
+          const bool two = r + 1 < ell;
+          const u32* K = Kstep + (size_t)pi * prime_words;
+          const u32* Kb0 = K + (size_t)((half * ell + r) * 2) * N;
+          const u32* Kb1 = Kb0 + 2 * N;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb0));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb0 + N));
+          if (two) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1 + N));
+          }
+          const int b = cc & 1;
+          mbar_wait(bars + b, (cc >> 1) & 1);
+          const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
+          fwd_consume<N, 2>(x, Xb + b * 2 * W, sl, tid, ft, R.p[pi], R.p2[pi], R.zero, bars + 2 + b);
+          cc++;
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            if (v == 1 && !two) break;
+            const u32* Kb = v ? Kb1 : Kb0;
+            const u32* Ka = Kb + N;
+            const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
+            const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
+            const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
+            const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              mb[k] += (u64)x[v][k] * kb[k];       // x < fwd_out_bound p, K < p: setup_rns checks that
+              ma[k] += (u64)x[v][k] * ka[k];       // 2 ell terms + the Montgomery term fit redc64
+            }
+          }
+        };
+        auto produce_inv = [&](int pi) {
+#pragma unroll
+          for (int k = 0; k < 8; k++) { x[0][k] = redc64(mb[k], R, pi); x[1][k] = redc64(ma[k], R, pi); }
+          const int b = cp & 1;
+          const uint4* it = R.itab + (size_t)pi * S::GROUPS * 4;
+          inv_produce<N, 2>(x, Xb + b * 2 * W, sl, tid, it, R.p[pi], R.p2[pi], R.zero, bars + 2 + b,
+                            ((cp >> 1) & 1) ^ 1, bars + b);
+          cp++;
+        };
+        auto consume_inv = [&](int pi) {
+          const int b = cc & 1;
+          mbar_wait(bars + b, (cc >> 1) & 1);
+          xload<N, 0, 2>(x, Xb + b * 2 * W, lay_base<N, 0>(tid), T);
+          warp_arrive(bars + 2 + b);
+          cc++;
+          const u32 pr = R.p[pi];
+          inv8_32<2>(x, R.itab + (size_t)pi * S::GROUPS * 4, pr, R.p2[pi], R.zero);
+          // CRT, accumulated prime by prime (see k_blind_rotate)
+#pragma unroll
+          for (int c = 0; c < 2; c++) {
+            u64* sa = sacc + c * N;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              const int pos = tid + T * k;
+              const u32 t = csub32(x[c][k], pr);
+              const u32 f = __umulhi(t, R.f16[pi]);
+              u64 a = sa[pos] + shoup64_28(t, R.M[pi], R.Ms32[pi], Q);
+              if (pi < NP - 1) {
+                a += (u64)f << 58;
+              } else {
+                const u32 kk = ((u32)(a >> 58) + f + 8) >> 4;
+                a &= (1ull << 58) - 1;
+                a += (u64)(NP + 1) * Q - (u64)kk * R.pq;
+                a = csub(a, Q << 3);
+                a = csub(a, Q << 2);
+                a = csub(a, Q << 1);
+                a = csub(a, Q);
+              }
+              sa[pos] = a;
+            }
+          }
+        };
+#pragma unroll
+        for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
+        produce_fwd(0, 0);
+#pragma unroll 1
+        for (int pi = 0; pi < NP; pi++) {
+#pragma unroll 1
+          for (int f = 0; f < NF; f++) {
+            if (f + 1 < NF) produce_fwd(pi, f + 1);
+            consume_fwd(pi, f);
+          }
+          produce_inv(pi);
+#pragma unroll
+          for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
+          if (pi + 1 < NP) produce_fwd(pi + 1, 0);
+          consume_inv(pi);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tslot), "n"(TCOLS));
 }
 
 // Latency variant for small batches: a cluster of NP x SPLIT CTAs per accumulator.  CTA rank
