@@ -39,6 +39,10 @@ struct fdfb_ctx {
   int br_cluster = 1;        // FDFB_BR_CLUSTER: 0 batched only, 1 auto (default), 2 / 3 force clusters of NP / 2 NP
   int imma_cg = 2;           // FDFB_IMMA_CG: int8 GEMM tiles per CTA pair (2, default) or per CTA (1)
   int br_kernel = 2;         // FDFB_BR_KERNEL: 2 pipelined k_blind_rotate_p (default), 1 k_blind_rotate
+  int boot_split = 1;        // FDFB_BOOT_SPLIT: 1 run the bootstrap as two stream-overlapped halves, 0 one part
+  cudaStream_t helper = nullptr;          // second stream of the two-part bootstrap (created at ctx_create)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  mutable std::mutex boot_mu;             // serialises the fork/join enqueue of concurrent callers
   int imma_wide_k = 65536;   // FDFB_IMMA_WIDE_K: K from which pair tiles are 448 columns wide
 };
 
@@ -662,6 +666,10 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
   if (const char* e = getenv("FDFB_IMMA_CG")) c->imma_cg = atoi(e) == 1 ? 1 : 2;
   if (const char* e = getenv("FDFB_BR_KERNEL")) c->br_kernel = atoi(e) == 1 ? 1 : 2;
+  if (const char* e = getenv("FDFB_BOOT_SPLIT")) c->boot_split = atoi(e) ? 1 : 0;
+  CK(cudaStreamCreateWithFlags(&c->helper, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   if (const char* e = getenv("FDFB_IMMA_WIDE_K")) c->imma_wide_k = atoi(e);
   DevParams& d = c->dp;
   memset(&d, 0, sizeof(d));
@@ -705,6 +713,9 @@ extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
   cudaFree(c->d_rtab);
+  if (c->helper) cudaStreamDestroy(c->helper);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   cudaSetDevice(cur);
 }
@@ -731,7 +742,7 @@ static const uint32_t kMaxBatch = 1u << 24;
 
 // workspace layout of fdfb_bootstrap_batch
 struct BootWs {
-  u32* abar; u32* bbar; u64* accs; u64* lweN; u64* dig; u64* F; void* ks; size_t bytes;
+  u32* abar; u32* bbar; u64* accs; u64* lweN; u64* dig; u64* F; void* ks; size_t ks_part; size_t bytes;
 };
 static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base, uint32_t k = 1) {
   BootWs w;
@@ -739,17 +750,19 @@ static BootWs boot_ws(const fdfb_params& p, uint32_t B, void* base, uint32_t k =
   size_t off = 0;
   auto take = [&](size_t bytes) { char* r = b + off; off += (bytes + 255) & ~(size_t)255; return r; };
   const size_t ellb = p.ell_boot, N = p.N;
-  const size_t nl = ellb > k ? ellb : k;                  // LWE_N samples alive at once (ladder or outputs)
+  const size_t nl = ellb + k;                             // LWE_N samples: ladder rows, then output rows
   w.abar = (u32*)take((size_t)B * p.n * 4);
   w.bbar = (u32*)take((size_t)B * 4);
   w.accs = (u64*)take((size_t)B * ellb * 2 * N * 8);
   w.lweN = (u64*)take((size_t)B * nl * (N + 1) * 8);
   w.dig = (u64*)take((size_t)B * ellb * N * 8);
   w.F = (u64*)take((size_t)B * k * 2 * N * 8);
-  {
-    const size_t kr = ks_ws_bytes(ks_shape_rlwe(p), (int)(B * ellb ? B * ellb : 1));
-    const size_t kl = ks_ws_bytes(ks_shape_lwe(p), (int)(B * k ? B * k : 1));
-    w.ks = take(kr > kl ? kr : kl);
+  {                                                       // one key-switch region per part (two parts)
+    const int half = (int)((B + 1) / 2);
+    const size_t kr = ks_ws_bytes(ks_shape_rlwe(p), (int)(half * ellb ? half * ellb : 1));
+    const size_t kl = ks_ws_bytes(ks_shape_lwe(p), (int)(half * k ? half * k : 1));
+    w.ks_part = align256(kr > kl ? kr : kl);
+    w.ks = take(2 * w.ks_part);
   }
   w.bytes = off;
   return w;
@@ -1097,16 +1110,74 @@ static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int 
   return FDFB_OK;
 }
 
+// Steps 3-7 of the bootstrap for ciphertexts [s0, s0 + cnt) of the batch (all workspace arrays
+// are indexed by ciphertext, so a part works on sub-ranges): ell_boot blind rotations of the part,
+// BuildAcc, the final rotation, extraction and the LWE key switch, on stream st.
+static int boot_part(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk, const uint64_t* rotp,
+                     uint32_t k, uint64_t* ct_out, uint32_t B, const BootWs& w, uint32_t s0, uint32_t cnt,
+                     void* ks_ws, cudaStream_t st) {
+  const fdfb_params& p = c->prm;
+  const int N = p.N, ellb = p.ell_boot;
+  if (cnt == 0) return FDFB_OK;
+  int rc;
+  size_t tot;
+  u64* accs = w.accs + (size_t)s0 * ellb * 2 * N;
+  u64* lad = w.lweN + (size_t)s0 * ellb * (N + 1);                 // ladder samples [B ell][N+1]
+  u64* dig = w.dig + (size_t)s0 * ellb * N;
+  const u32* abar = w.abar + (size_t)s0 * p.n;
+  const u32* bbar = w.bbar + s0;
+  // 3. ell_boot blind rotations of every ciphertext, batched      (PAPER.md:2217)
+  if ((rc = launch_br(c, (const u64*)brk, accs, (int)(cnt * ellb), ellb, abar, st))) return rc;
+  // 4. SampleExt(., 1) + L^{i-1}/2                                (PAPER.md:2218)
+  tot = (size_t)cnt * ellb * (N + 1);
+  k_ladder_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, accs, (int)(cnt * ellb), lad);
+  CKL(c);
+  // 5. BuildAcc: KeySwitch LWE->RLWE (into accs), then PubMux per LUT (PAPER.md:2181-2191, 2221)
+  if ((rc = keyswitch_rlwe(c, (const u64*)bpk, lad, (int)(cnt * ellb), accs, ks_ws, st))) return rc;
+  if ((rc = launch_ntt_batch(c, accs, (size_t)cnt * ellb * 2, 0, st))) return rc;
+  for (uint32_t kk = 0; kk < k; kk++) {
+    const uint64_t* rp = rotp + (size_t)kk * 2 * N;
+    u64* F = w.F + ((size_t)kk * B + s0) * 2 * N;
+    tot = (size_t)cnt * N;
+    k_pubmux_digits<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rp, bbar, (int)cnt, dig);
+    CKL(c);
+    if ((rc = launch_ntt_batch(c, dig, (size_t)cnt * ellb, 0, st))) return rc;
+    tot = (size_t)cnt * 2 * N;
+    k_pubmux_mac<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, dig, accs, (int)cnt, F, c->qinv_neg, c->r2);
+    CKL(c);
+    if ((rc = launch_ntt_batch(c, F, (size_t)cnt * 2, 1, st))) return rc;
+    tot = (size_t)cnt * N;
+    k_pubmux_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rp, bbar, (int)cnt, F);
+    CKL(c);
+  }
+  // 6.-7. final blind rotation, SampleExt(., 1), ModSwitch(Q -> q_lwe), KeySwitch mod q_lwe
+  //       (reading c.3); output samples after the ladder rows
+  for (uint32_t kk = 0; kk < k; kk++) {
+    u64* F = w.F + ((size_t)kk * B + s0) * 2 * N;
+    u64* o = w.lweN + ((size_t)ellb * B + (size_t)kk * B + s0) * (N + 1);
+    if ((rc = launch_br(c, (const u64*)brk, F, (int)cnt, 1, abar, st, (int)cnt))) return rc;
+    tot = (size_t)cnt * (N + 1);
+    k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, F, (int)cnt, o);
+    CKL(c);
+    if ((rc = keyswitch_lwe(c, (const u64*)ksk, o, (int)cnt, ct_out + ((size_t)kk * B + s0) * (p.n + 1), ks_ws, st)))
+      return rc;
+  }
+  return FDFB_OK;
+}
+
 // FDFB Bootstrap (Fig. Bootstrap; readings R1, F4, c.3) of B ciphertexts
 // under k LUTs (rotp: k x [2][N]); the ladder rotations, SampleExt and the LWE->RLWE key
 // switch are shared by the k functions; out: [k][B][n+1].
+// Large single-LUT batches run as two halves, the second on the context's helper stream (forked
+// and joined with events, so the call stays stream-ordered and graph-capturable): the blind
+// rotations of one half fill the SMs the other half's persistent CTAs leave idle at the end of
+// each launch (the wave tail), and one half's BuildAcc / key switches overlap the other's BR.
 static int bootstrap_impl(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk, const uint64_t* rotp,
                           uint32_t k, const uint64_t* ct_in, uint64_t* ct_out, uint32_t B, void* workspace,
                           cudaStream_t st) {
   const fdfb_params& p = c->prm;
   const int N = p.N, ellb = p.ell_boot;
   BootWs w = boot_ws(p, B, workspace, k);
-  int rc;
   size_t tot;
   // 1. ModSwitch(ct, q_lwe, 2N)
   tot = (size_t)B * (p.n + 1);
@@ -1116,37 +1187,19 @@ static int bootstrap_impl(const fdfb_ctx* c, const void* brk, const void* bpk, c
   tot = (size_t)B * ellb * N;
   k_ladder_init<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.bbar, B, w.accs);
   CKL(c);
-  // 3. ell_boot blind rotations of every ciphertext, batched      (PAPER.md:2217)
-  if ((rc = launch_br(c, (const u64*)brk, w.accs, (int)(B * ellb), ellb, w.abar, st))) return rc;
-  // 4. SampleExt(., 1) + L^{i-1}/2                                (PAPER.md:2218)
-  tot = (size_t)B * ellb * (N + 1);
-  k_ladder_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.accs, B * ellb, w.lweN);
-  CKL(c);
-  // 5. BuildAcc: KeySwitch LWE->RLWE (into accs), then PubMux per LUT (PAPER.md:2181-2191, 2221)
-  if ((rc = keyswitch_rlwe(c, (const u64*)bpk, w.lweN, (int)(B * ellb), w.accs, w.ks, st))) return rc;
-  if ((rc = launch_ntt_batch(c, w.accs, (size_t)B * ellb * 2, 0, st))) return rc;
-  for (uint32_t kk = 0; kk < k; kk++) {
-    const uint64_t* rp = rotp + (size_t)kk * 2 * N;
-    u64* F = w.F + (size_t)kk * B * 2 * N;
-    tot = (size_t)B * N;
-    k_pubmux_digits<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rp, w.bbar, B, w.dig);
-    CKL(c);
-    if ((rc = launch_ntt_batch(c, w.dig, (size_t)B * ellb, 0, st))) return rc;
-    tot = (size_t)B * 2 * N;
-    k_pubmux_mac<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.dig, w.accs, B, F, c->qinv_neg, c->r2);
-    CKL(c);
-    if ((rc = launch_ntt_batch(c, F, (size_t)B * 2, 1, st))) return rc;
-    tot = (size_t)B * N;
-    k_pubmux_finish<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, rp, w.bbar, B, F);
-    CKL(c);
-  }
-  // 6. final blind rotation of all k*B accumulators in one launch
-  if ((rc = launch_br(c, (const u64*)brk, w.F, (int)(k * B), 1, w.abar, st, (int)B))) return rc;
-  // 7. SampleExt(., 1), ModSwitch(Q -> q_lwe), KeySwitch mod q_lwe (reading c.3)
-  tot = (size_t)k * B * (N + 1);
-  k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, w.F, (int)(k * B), w.lweN);
-  CKL(c);
-  return keyswitch_lwe(c, (const u64*)ksk, w.lweN, (int)(k * B), ct_out, w.ks, st);
+  void* ks0 = w.ks;
+  void* ks1 = (char*)w.ks + w.ks_part;
+  const bool split = c->boot_split && k == 1 && B >= 64;
+  if (!split) return boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, 0, B, ks0, st);
+  const uint32_t h = B / 2;
+  std::lock_guard<std::mutex> lock(c->boot_mu);
+  CK(cudaEventRecord(c->ev_fork, st));
+  CK(cudaStreamWaitEvent(c->helper, c->ev_fork, 0));
+  int rc = boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, 0, h, ks0, st);
+  int rc2 = boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, h, B - h, ks1, c->helper);
+  CK(cudaEventRecord(c->ev_join, c->helper));
+  CK(cudaStreamWaitEvent(st, c->ev_join, 0));
+  return rc ? rc : rc2;
 }
 
 extern "C" int fdfb_bootstrap_batch(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk,

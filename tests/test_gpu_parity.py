@@ -740,3 +740,37 @@ def test_empty_batches_are_noops():
     torch.cuda.synchronize()
     assert pctx.launch_count() == n1
     pctx.device_status()
+
+
+def test_bootstrap_two_part_split_equals_one_part_and_oracle(monkeypatch):
+    """B >= 64 single-LUT batches run as two stream-overlapped halves (helper stream forked and
+    joined with events): bytes equal the one-part run (FDFB_BOOT_SPLIT=0) and the oracle on a
+    seeded sample, also when the split call is captured into a CUDA graph and replayed."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    f = synth.lut(cfg, seed=91)
+    rotp = orc.setup_polynomial(orc.bootsmap(f))
+    rot = ctx.setup_lut(f)
+    B = 201                                                     # odd: halves of 100 and 101
+    cts = orc.lwe_encrypt(92, K["s"], synth.messages(cfg, B, seed=93))
+    got = H(ctx.bootstrap_batch(dk, rot, T(cts)))
+    monkeypatch.setenv("FDFB_BOOT_SPLIT", "0")
+    one = Context(cfg, 0)
+    dk1 = {"brk": one.key_import(KEY_BRK, T(K["brk"].reshape(-1))),
+           "bpk": one.key_import(KEY_BPK, T(K["bpk"].reshape(-1))),
+           "ksk": one.key_import(KEY_KSK, T(K["ksk"].reshape(-1)))}
+    assert np.array_equal(got, H(one.bootstrap_batch(dk1, one.setup_lut(f), T(cts))))
+    pick = np.sort(np.random.default_rng(94).choice(B, 12, replace=False))
+    assert np.array_equal(got[pick], orc.bootstrap(K, rotp, cts[pick]))
+    ws = ctx.workspace_bootstrap(B)
+    static_in = T(cts)
+    out = torch.empty_like(static_in)
+    ctx.bootstrap_batch(dk, rot, static_in, out, ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.bootstrap_batch(dk, rot, static_in, out, ws)
+    other = orc.lwe_encrypt(95, K["s"], synth.messages(cfg, B, seed=96))
+    static_in.copy_(T(other))
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ctx.bootstrap_batch(dk, rot, T(other)))
