@@ -45,10 +45,18 @@ def imad_per_modmul(cfg):
     """Slots of one direct lazy Shoup modmul at the configuration's word size: 16 for a 54-bit
     Q (above), 4 for Q < 2^32 (IMAD.HI + 2 IMAD on 32-bit words)."""
     return IMAD_PER_MODMUL if cfg["Q"] >= (1 << 32) else 4
-# DRAM traffic of k_blind_rotate<2048,3> per wave of 296 resident accumulators (2 per SM), from
-# `ncu --set full` (dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/ncu_full_blind_rotate.txt):
-# the RNS brK (0.81 GB) streams about twice per wave; the kernel is integer-pipe bound.
-BR_DRAM_BYTES_PER_WAVE = 1.5734e9 + 0.0121e9
+# DRAM traffic of one bench step, measured: `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum`
+# over every launch of one step of this workload (tools/traffic_step.py; the summary JSON is
+# committed under profiles/<round>/traffic_<workload>.json and read at run time).  None if absent.
+TRAFFIC_FILES = [os.path.join(ROOT, "profiles", r, "traffic_%s.json") for r in ("r02", "r01")]
+
+
+def measured_traffic(workload):
+    for f in TRAFFIC_FILES:
+        f = f % workload
+        if os.path.exists(f):
+            return json.load(open(f))
+    return None
 
 
 def parse():
@@ -226,7 +234,7 @@ class BootstrapWorkload:
     metric = "functional bootstraps/sec (N=2048)"
     unit = "bootstraps/s"
     kclass = "blind_rotate"
-    kernel = "k_blind_rotate<2048,3>"
+    kernel = "k_blind_rotate_p<2048,3>"
 
     def __init__(self, ctx, cfg, B, rank, world, dev, stream):
         import torch
@@ -291,16 +299,18 @@ class BootstrapWorkload:
         modmul_step = per_cmux * cmux_per_bs * self.B
         imad_s = modmul_step * imad_per_modmul(self.cfg) / (kernel_ms_per_step / 1e3)
         peak = 148 * IMAD_PER_SM_CLK * 1965e6
-        waves = self.B * (self.cfg["ell_boot"] + 1) / 296.0
         hbm_peak = json.load(open(PEAKS_FILE))["hbm_gbs"] if os.path.exists(PEAKS_FILE) else 6549.8
-        hbm_gbs = BR_DRAM_BYTES_PER_WAVE * waves / (kernel_ms_per_step / 1e3) / 1e9
+        tr = measured_traffic("bootstrap") if self.B == 4096 else None
+        traffic = tr["dram_bytes_per_step"] if tr else None
+        hbm_gbs = traffic / (ms_step / 1e3) / 1e9 if traffic else None
         return {"kernel": self.kernel, "bound": "alu", "achieved": imad_s / 1e12, "peak": peak / 1e12,
                 "unit": "T IMAD-slots/s", "frac": imad_s / peak,
-                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
-                        "basis": "key-stream DRAM bytes (ncu) / BR time vs MEASURED_PEAKS.json hbm_gbs"},
-                "traffic": BR_DRAM_BYTES_PER_WAVE * waves,
-                "traffic_basis": "ncu dram bytes of one 296-accumulator wave x waves per step "
-                                 "(brK re-streamed per wave; 0.2% of HBM bandwidth, not the bound)",
+                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak,
+                        "frac": hbm_gbs / hbm_peak if hbm_gbs else None,
+                        "basis": "measured DRAM bytes of one step (ncu) / step time vs MEASURED_PEAKS.json hbm_gbs"},
+                "traffic": traffic,
+                "traffic_basis": (tr["how"] + "; " + tr["source"]) if tr else "not measured for this batch",
+                "algorithmic_bytes_per_step": self.B * 2 * (self.cfg["n"] + 1) * 8 + self.key_bytes,
                 "modmul_per_step": modmul_step, "imad_per_modmul": imad_per_modmul(self.cfg),
                 "modmul_per_s": modmul_step / (kernel_ms_per_step / 1e3),
                 "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; "
@@ -733,7 +743,7 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in evs)
     k_ms, k_launches = 0.0, 0
     for kc in kcls:
-        a_ms, a_n = ctx.timing_read(kc)
+        a_ms, a_n = ctx.timing_read(kc, union=True)     # span covered (the halves' launches overlap)
         k_ms, k_launches = k_ms + a_ms, k_launches + a_n
     ctx.timing_enable(False)
     if world > 1:

@@ -280,6 +280,9 @@ enum { FDFB_KCLASS_BLIND_ROTATE = 0, FDFB_KCLASS_KEYSWITCH_RLWE = 1, FDFB_KCLASS
        FDFB_KCLASS_SHIFT = 3, FDFB_KCLASS_SHIFT_GEMM = 4 };
 int fdfb_timing_enable(const fdfb_ctx* ctx, int on);
 int fdfb_timing_read(const fdfb_ctx* ctx, int kclass, double* total_ms, uint64_t* launches);
+/* As fdfb_timing_read, but *union_ms is the span covered by the launches (the union of their
+ * [start, end] intervals): launches of one call on two streams may overlap. */
+int fdfb_timing_read_union(const fdfb_ctx* ctx, int kclass, double* union_ms, uint64_t* launches);
 /* Device-side argument errors of earlier stream-ordered calls: synchronises, returns
  * FDFB_E_INDEX if any kernel saw an out-of-range k/d since the last clear, else FDFB_OK. */
 int fdfb_device_status(const fdfb_ctx* ctx, int clear);

@@ -2,6 +2,7 @@
 // context setup (roots of unity, twiddles, CDT), key generation/import and the
 // stream-ordered orchestration of the hot-path kernels.  Unity build: the kernel
 // headers are included here.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -1397,6 +1398,35 @@ extern "C" int fdfb_timing_read(const fdfb_ctx* c, int kclass, double* total_ms,
   }
   c->tev.swap(keep);
   *total_ms = ms; *launches = cnt;
+  return FDFB_OK;
+}
+// Wall span covered by the launches of one class: the union of their [start, end] intervals
+// (launches on the bootstrap's two streams overlap, so their summed durations overcount).
+extern "C" int fdfb_timing_read_union(const fdfb_ctx* c, int kclass, double* union_ms, uint64_t* launches) {
+  if (!c || !union_ms || !launches) return FDFB_E_NULL;
+  std::lock_guard<std::mutex> g(c->tmu);
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep, mine;
+  for (auto& e : c->tev) (e.first == kclass ? mine : keep).push_back(e);
+  std::vector<std::pair<double, double>> iv;
+  for (auto& e : mine) CK(cudaEventSynchronize(e.second.second));
+  for (auto& e : mine) {
+    float a = 0, b = 0;
+    CK(cudaEventElapsedTime(&a, mine[0].second.first, e.second.first));   // may be negative
+    CK(cudaEventElapsedTime(&b, mine[0].second.first, e.second.second));
+    iv.push_back({a, b});
+  }
+  std::sort(iv.begin(), iv.end());
+  double ms = 0, cs = 0, ce = 0;
+  bool open = false;
+  for (auto& x : iv) {
+    if (!open || x.first > ce) { if (open) ms += ce - cs; cs = x.first; ce = x.second; open = true; }
+    else if (x.second > ce) ce = x.second;
+  }
+  if (open) ms += ce - cs;
+  for (auto& e : mine) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+  c->tev.swap(keep);
+  *union_ms = ms;
+  *launches = mine.size();
   return FDFB_OK;
 }
 extern "C" uint64_t fdfb_launch_count(const fdfb_ctx* c) { return c ? (uint64_t)c->launches.load() : 0; }

@@ -46,7 +46,8 @@ _EXPORTS = ["fdfb_ctx_create", "fdfb_ctx_destroy", "fdfb_sizes", "fdfb_workspace
             "fdfb_bootstrap_tfhe_batch", "fdfb_workspace_permute", "fdfb_permute",
             "fdfb_workspace_bootstrap_shift", "fdfb_bootstrap_shift_batch", "fdfb_lwe_decrypt", "fdfb_rlwe_phase",
             "fdfb_gemm_i8", "fdfb_workspace_keygen", "fdfb_workspace_keygen_canonical",
-            "fdfb_workspace_rlwe_encrypt", "fdfb_workspace_poly_mul", "fdfb_workspace_rlwe_phase"]
+            "fdfb_workspace_rlwe_encrypt", "fdfb_workspace_poly_mul", "fdfb_workspace_rlwe_phase",
+            "fdfb_timing_read_union"]
 KCLASS = {"blind_rotate": 0, "keyswitch_rlwe": 1, "keyswitch_lwe": 2, "shift": 3, "shift_gemm": 4}
 
 
@@ -120,6 +121,7 @@ def lib():
         L.fdfb_pack.argtypes = [vp, vp, vp, vp, vp, u32, vp]
         L.fdfb_device_status.argtypes = [vp, C.c_int]
         L.fdfb_timing_read.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(u64)]
+        L.fdfb_timing_read_union.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(u64)]
         _lib = L
     return _lib
 
@@ -211,10 +213,12 @@ class Context:
     def timing_enable(self, on: bool = True):
         _check(lib().fdfb_timing_enable(self.h, 1 if on else 0))
 
-    def timing_read(self, kclass: str):
-        """(summed device ms, launches) of one kernel class since the last read."""
+    def timing_read(self, kclass: str, union: bool = False):
+        """(device ms, launches) of one kernel class since the last read: summed durations, or with
+        union=True the span the launches cover (launches on two streams may overlap)."""
         ms, cnt = C.c_double(), C.c_uint64()
-        _check(lib().fdfb_timing_read(self.h, KCLASS[kclass], C.byref(ms), C.byref(cnt)))
+        f = lib().fdfb_timing_read_union if union else lib().fdfb_timing_read
+        _check(f(self.h, KCLASS[kclass], C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
 
     # ---------------------------------------------------------------- keys
