@@ -616,7 +616,12 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5;
   const u64 Q = p.Q;
-  const int ell = p.ell_rgsw, logL = p.logL_rgsw, u = p.u;
+#ifdef FDFB_EXP_UNROLLF
+  constexpr int ell = 4;
+#else
+  const int ell = p.ell_rgsw;
+#endif
+  const int logL = p.logL_rgsw, u = p.u;
   const u32 dmask = (1u << logL) - 1;
   const int PPH = (ell + 1) / 2;                   // digit pairs per half
   const int NF = 2 * PPH;                          // forward transforms per prime
@@ -787,9 +792,13 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
 #pragma unroll
         for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
         produce_fwd(0, 0);
+#pragma unroll
+        for (int pi = 0; pi < NP; pi++) {          // unrolled: per-prime constants from the parameter bank
+#ifdef FDFB_EXP_UNROLLF
+#pragma unroll
+#else
 #pragma unroll 1
-        for (int pi = 0; pi < NP; pi++) {
-#pragma unroll 1
+#endif
           for (int f = 0; f < NF; f++) {
             if (f + 1 < NF) produce_fwd(pi, f + 1);
             consume_fwd(pi, f);

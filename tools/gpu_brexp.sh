@@ -24,6 +24,8 @@ for v in "$@"; do
     nobar) run nobar -DFDFB_EXP_NOBAR=1 ;;
     nod) run nod -DFDFB_EXP_NOD=1 ;;
     nocsub) run nocsub -DFDFB_EXP_NOCSUB=1 ;;
+    unrollp) run unrollp -DFDFB_EXP_UNROLLP=1 ;;
+    unrollf) run unrollf -DFDFB_EXP_UNROLLF=1 ;;
     *) tag=$(echo $v | tr -c 'a-zA-Z0-9' '_'); run $tag $v ;;
   esac
 done
