@@ -232,7 +232,7 @@ static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, 
                        const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
   constexpr int T = N / 8;
   if (c->br_kernel != 1) {                     // pipelined kernel (mbarrier-decoupled exchanges, d in TMEM)
-    const size_t sm = 43 * (size_t)N;          // acc 16N + X0/X1 18N + slabs 9N
+    const size_t sm = (25 + 9 * BR_NB) * (size_t)N;   // acc 16N + NB cross-warp buffers 9N each + slabs 9N
     cudaFuncSetAttribute(k_blind_rotate_p<N, NP, GIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_blind_rotate_p<N, NP, GIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);

@@ -552,13 +552,13 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 // (F: forward digit-pair transforms of a prime, I: its inverse; ' = next prime).
 // one arrival per warp: __syncwarp orders the lanes' shared-memory accesses before lane 0's
 // (release) arrive, so the barriers count warps, not threads
-FDFB_DEV void warp_arrive(uint64_t* b) {
+FDFB_DEV void warp_arrive(uint32_t baddr) {
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(b);
+  if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(baddr) : "memory");
 }
 template <int N, int V>
 FDFB_DEV void fwd_consume(u32 (&x)[V][8], const u32* X, u32* sl, int tid, const uint4* tab, u32 p, u32 p2, u32 z,
-                          uint64_t* empty_b) {
+                          uint32_t empty_b) {
   using S = BrShape<N>;
   constexpr int T1 = N >> 6;                       // pass-1 stride
   const int B = qbase<N, 1>(tid);
@@ -582,7 +582,7 @@ FDFB_DEV void fwd_consume(u32 (&x)[V][8], const u32* X, u32* sl, int tid, const 
 // slab, pass 1 -> layout 0 into X[b]
 template <int N, int V>
 FDFB_DEV void inv_produce(u32 (&x)[V][8], u32* X, u32* sl, int tid, const uint4* tab, u32 p, u32 p2, u32 z,
-                          uint64_t* empty_b, uint32_t empty_par, uint64_t* full_b) {
+                          uint32_t empty_b, uint32_t empty_par, uint32_t full_b) {
   using S = BrShape<N>;
   constexpr int NM = S::NMID;
   inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
@@ -594,11 +594,17 @@ FDFB_DEV void inv_produce(u32 (&x)[V][8], u32* X, u32* sl, int tid, const uint4*
   const int B = qbase<N, 1>(tid);
   xload<N, 1, V>(x, sl, lay_base<N, 1>(B), T1);
   inv8_32<V>(x, tab + 4 * (S::grp(1) + tid / T1), p, p2, z);
-  mbar_wait(empty_b, empty_par);
+  mbar_wait_sleep(empty_b, empty_par);
   xstore<N, 0, V>(x, X, lay_base<N, 0>(B), T1);
   warp_arrive(full_b);
 }
 
+#ifndef BR_NB
+#define BR_NB 3      // cross-warp exchange buffers of k_blind_rotate_p
+#endif
+#ifndef BR_LA
+#define BR_LA 2      // transforms produced ahead of the one consumed (<= BR_NB - 1)
+#endif
 template <int N, int NP, bool GIN>
 __global__ void __launch_bounds__(N / 8, BrShape<N>::MINB)
 k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
@@ -611,8 +617,8 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   extern __shared__ u64 smem[];
   u64* sacc = smem;                                // [b | a], natural order, canonical mod Q
   u32* Xb = (u32*)(smem + 2 * N);                  // X0, X1: 2 planes of W words each
-  u32* sl = Xb + 2 * 2 * W;                        // warp-local exchange slabs (2 planes of W words)
-  __shared__ uint64_t bars[4];                     // full[0..1], empty[2..3]
+  u32* sl = Xb + BR_NB * 2 * W;                    // warp-local exchange slabs (2 planes of W words)
+  __shared__ uint64_t bars[2 * BR_NB];             // full[0 .. NB-1], empty[NB .. 2 NB-1]
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5;
   const u64 Q = p.Q;
@@ -628,7 +634,7 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   const size_t prime_words = (size_t)2 * ell * 2 * N;
   const size_t step_words = (size_t)NP * prime_words;
   if (tid == 0) {
-    for (int b = 0; b < 4; b++) mbar_init(bars + b, T / 32);   // one arrival per warp
+    for (int b = 0; b < 2 * BR_NB; b++) mbar_init(bars + b, T / 32);   // one arrival per warp
   }
   constexpr int TCOLS = T > 128 ? 64 : 32;         // 32 words per thread; warps w, w + 4 share lanes
   if (warp == 0) {
@@ -641,7 +647,10 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   tc_fence_after();
   // this thread's 32 TMEM words: lanes 32 (warp % 4) .., column group warp / 4
   const uint32_t tm = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
-  int cp = 0, cc = 0;                              // produced / consumed transform counters (uniform)
+  const uint32_t bar0 = smem_u32(bars);            // full[b] = bar0 + 8 b, empty[b] = bar0 + 8 NB + 8 b
+  constexpr uint32_t EO = 8 * BR_NB;
+  int cpb = 0, ccb = 0;                            // buffer of the next produced / consumed transform
+  uint32_t cpp = 0, ccp = 0;                       // and its use parity (flips when the buffer index wraps)
   u32 x[2][8];
   u64 mb[8], ma[8];
 
@@ -708,11 +717,11 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
           }
           const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
           fwd8_32<2>(x, ft, R.p[pi], R.p2[pi], R.zero);          // pass 0 (inputs < 2p)
-          const int b = cp & 1;
-          mbar_wait(bars + 2 + b, ((cp >> 1) & 1) ^ 1);
+          const int b = cpb;
+          mbar_wait_sleep(bar0 + EO + 8 * b, cpp ^ 1);
           xstore<N, 0, 2>(x, Xb + b * 2 * W, lay_base<N, 0>(tid), T);
-          warp_arrive(bars + b);
-          cp++;
+          warp_arrive(bar0 + 8 * b);
+          if (++cpb == BR_NB) { cpb = 0; cpp ^= 1; }
         };
         auto consume_fwd = [&](int pi, int f) {
           const int half = f >= PPH ? 1 : 0, r = 2 * (f - half * PPH);   // f < 2 PPH: no division
@@ -726,11 +735,11 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
             asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1 + N));
           }
-          const int b = cc & 1;
-          mbar_wait(bars + b, (cc >> 1) & 1);
+          const int b = ccb;
+          mbar_wait_sleep(bar0 + 8 * b, ccp);
           const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
-          fwd_consume<N, 2>(x, Xb + b * 2 * W, sl, tid, ft, R.p[pi], R.p2[pi], R.zero, bars + 2 + b);
-          cc++;
+          fwd_consume<N, 2>(x, Xb + b * 2 * W, sl, tid, ft, R.p[pi], R.p2[pi], R.zero, bar0 + EO + 8 * b);
+          if (++ccb == BR_NB) { ccb = 0; ccp ^= 1; }
 #pragma unroll
           for (int v = 0; v < 2; v++) {
             if (v == 1 && !two) break;
@@ -750,18 +759,18 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
         auto produce_inv = [&](int pi) {
 #pragma unroll
           for (int k = 0; k < 8; k++) { x[0][k] = redc64(mb[k], R, pi); x[1][k] = redc64(ma[k], R, pi); }
-          const int b = cp & 1;
+          const int b = cpb;
           const uint4* it = R.itab + (size_t)pi * S::GROUPS * 4;
-          inv_produce<N, 2>(x, Xb + b * 2 * W, sl, tid, it, R.p[pi], R.p2[pi], R.zero, bars + 2 + b,
-                            ((cp >> 1) & 1) ^ 1, bars + b);
-          cp++;
+          inv_produce<N, 2>(x, Xb + b * 2 * W, sl, tid, it, R.p[pi], R.p2[pi], R.zero, bar0 + EO + 8 * b, cpp ^ 1,
+                            bar0 + 8 * b);
+          if (++cpb == BR_NB) { cpb = 0; cpp ^= 1; }
         };
         auto consume_inv = [&](int pi) {
-          const int b = cc & 1;
-          mbar_wait(bars + b, (cc >> 1) & 1);
+          const int b = ccb;
+          mbar_wait_sleep(bar0 + 8 * b, ccp);
           xload<N, 0, 2>(x, Xb + b * 2 * W, lay_base<N, 0>(tid), T);
-          warp_arrive(bars + 2 + b);
-          cc++;
+          warp_arrive(bar0 + EO + 8 * b);
+          if (++ccb == BR_NB) { ccb = 0; ccp ^= 1; }
           const u32 pr = R.p[pi];
           inv8_32<2>(x, R.itab + (size_t)pi * S::GROUPS * 4, pr, R.p2[pi], R.zero);
           // CRT, accumulated prime by prime (see k_blind_rotate)
@@ -791,7 +800,11 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
         };
 #pragma unroll
         for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
-        produce_fwd(0, 0);
+        // lookahead BR_LA transforms (BR_LA <= BR_NB - 1): forward transforms are independent of
+        // each other; the inverse of a prime needs its last forward transform consumed (the MAC)
+#pragma unroll
+        for (int f = 0; f < BR_LA; f++)
+          if (f < NF) produce_fwd(0, f);
 #pragma unroll
         for (int pi = 0; pi < NP; pi++) {          // unrolled: per-prime constants from the parameter bank
 #ifdef FDFB_EXP_UNROLLF
@@ -800,13 +813,17 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
 #pragma unroll 1
 #endif
           for (int f = 0; f < NF; f++) {
-            if (f + 1 < NF) produce_fwd(pi, f + 1);
+            if (f + BR_LA < NF) produce_fwd(pi, f + BR_LA);
             consume_fwd(pi, f);
           }
           produce_inv(pi);
 #pragma unroll
           for (int k = 0; k < 8; k++) { mb[k] = 0; ma[k] = 0; }
-          if (pi + 1 < NP) produce_fwd(pi + 1, 0);
+          if (pi + 1 < NP) {
+#pragma unroll
+            for (int f = 0; f < BR_LA; f++)
+              if (f < NF) produce_fwd(pi + 1, f);
+          }
           consume_inv(pi);
         }
       }

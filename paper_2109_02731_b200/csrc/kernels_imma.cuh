@@ -89,6 +89,18 @@ FDFB_DEV void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// as mbar_wait, with a suspend-time hint: the waiting warp sleeps until the phase completes (or
+// the hint, in ns, expires) instead of re-polling, so waiting warps take no issue slots from
+// the ones doing arithmetic
+FDFB_DEV void mbar_wait_sleep(uint32_t baddr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(baddr),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 FDFB_DEV void tma_load_2d(const CUtensorMap* tm, void* dst, uint64_t* bar, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(

@@ -26,6 +26,8 @@ for v in "$@"; do
     nocsub) run nocsub -DFDFB_EXP_NOCSUB=1 ;;
     unrollp) run unrollp -DFDFB_EXP_UNROLLP=1 ;;
     unrollf) run unrollf -DFDFB_EXP_UNROLLF=1 ;;
+    nb3la1) run nb3la1 -DBR_NB=3 -DBR_LA=1 ;;
+    nb3la2) run nb3la2 -DBR_NB=3 -DBR_LA=2 ;;
     *) tag=$(echo $v | tr -c 'a-zA-Z0-9' '_'); run $tag $v ;;
   esac
 done

@@ -1,6 +1,7 @@
 """Per-source-line warp-stall samples of one kernel from an ncu report (--import-source on).
 
     python tools/ncu_lines.py REPORT.ncu-rep MANGLED_KERNEL_NAME [TOP]
+    (NCU_LINES_METRIC=<source-page column>, e.g. "Instructions Executed", sums that column instead)
 
 Compiles csrc/fdfb_api.cu to a cubin with -lineinfo (same flags as the library), maps every
 SASS offset of the kernel to its (file, line) with nvdisasm -g, and sums the report's
@@ -38,13 +39,13 @@ def main(rep, fn, top=40):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))
     h = rows[1]
-    ai, wi = h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
+    ai, wi = h.index("Address"), h.index(os.environ.get("NCU_LINES_METRIC", "Warp Stall Sampling (All Samples)"))
     base, agg, tot = None, collections.Counter(), 0
     for r in rows[2:]:
         if len(r) <= wi:
             continue
         try:
-            a, w = int(r[ai], 16), int(r[wi])
+            a, w = int(r[ai], 16), int(float(r[wi] or 0))
         except ValueError:
             continue
         base = a if base is None else base
