@@ -15,8 +15,9 @@
  *     except FDFB_E_CUDA (a launch or runtime call failed; see
  *     fdfb_last_cuda_error).  Nothing throws across the ABI.
  *   - A batch count of 0 (B, count) returns FDFB_OK before any other check except
- *     the context: its data pointers may then be NULL (empty tensors).  The bootstrap
- *     entry points accept B <= 2^24 per call (FDFB_E_DIMENSION above).
+ *     the context: its data pointers may then be NULL (empty tensors).  The FDFB / TFHE
+ *     bootstrap entry points accept B <= 2^24 per call, Shift, RLWE encryption and the
+ *     shift-based bootstrap B <= 65535 (FDFB_E_DIMENSION above).
  *   - Calls run on the CUDA device that is current in the calling thread; it must be the
  *     context's device (one process or thread per GPU, as bench.py and dist.py do).
  *   - Ciphertext layouts (canonical, coefficient domain, residues canonical):

@@ -401,9 +401,9 @@ static KsGemm ks_shape_rlwe(const fdfb_params& p) { return ks_gemm_shape(p.N, p.
 static KsGemm ks_shape_lwe(const fdfb_params& p) { return ks_gemm_shape(p.N, p.ell_ks, p.logL_ks, p.n + 1); }
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static const size_t kKsABytes = 1ull << 30;     // int8 limb-matrix chunk cap
-static int ks_chunk_rows(const KsGemm& g) {     // LWE samples per GEMM chunk
+static int ks_chunk_rows(const KsGemm& g) {     // LWE samples per GEMM chunk (<= 32768: k_ks_gemm_bits grid.y)
   size_t r = kKsABytes / ((size_t)g.NLP * g.Kd);
-  return (int)(r < 1 ? 1 : (r > (1 << 20) ? (1 << 20) : r));
+  return (int)(r < 1 ? 1 : (r > (1 << 15) ? (1 << 15) : r));
 }
 static size_t ks_ws_bytes(const KsGemm& g, int count) {
   const int rows = count < ks_chunk_rows(g) ? count : ks_chunk_rows(g);
@@ -1028,6 +1028,7 @@ extern "C" int fdfb_rlwe_encrypt(const fdfb_ctx* c, uint64_t seed, const int8_t*
                                  uint32_t count, uint64_t first_index, uint64_t* out, void* workspace, void* stream) {
   if (!c) return FDFB_E_NULL;
   if (!count) return FDFB_OK;  // empty batch: data pointers may be NULL
+  if (count > 65535) return FDFB_E_DIMENSION;   // one grid row per ciphertext
   if (!sk_rlwe || !msg || !out) return FDFB_E_NULL;
   if (!workspace) return FDFB_E_WORKSPACE;
   cudaStream_t st = S(stream);
