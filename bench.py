@@ -406,11 +406,25 @@ class ShiftWorkload:
         K = ell * (N - 1) + N + ell * N
         ops = 2.0 * (2 * self.B) * K * (7 * 2 * N)
         tops = ops / (kernel_ms_per_step / 1e3) / 1e12
-        bf16 = json.load(open(PEAKS_FILE))["bf16_tflops"] if os.path.exists(PEAKS_FILE) else 1590.0
+        pk = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+        # the burst peak for a short timed region, the sustained (power-capped) one for a long one
+        sustained = getattr(self, "timed_ms", 0) > 1000.0 and "bf16_tflops_sustained" in pk
+        bf16 = pk.get("bf16_tflops_sustained" if sustained else "bf16_tflops", 1590.0)
         peak = 2 * bf16
+        # the suffix-sum route is ~4 N^2 ell bit-selected modular additions per shift;
+        # on CUDA cores one 64-bit modular add is >= 5 ALU lane-ops (IADD3, IADD3.X, ISETP.EX x2, SEL)
+        modadds = 4.0 * N * N * ell * self.B
+        alu_peak = 148 * 64 * 1965e6 / 5
         return {"kernel": self.kernel, "bound": "tensor", "achieved": tops, "peak": peak, "unit": "TOP/s (int8)",
                 "frac": tops / peak, "traffic": None, "gemm": {"M": 2 * self.B, "K": K, "N": 7 * 2 * N},
-                "peak_basis": "2 x MEASURED_PEAKS.json bf16_tflops (int8 = 2 x bf16 nominal)"}
+                "peak_basis": "2 x MEASURED_PEAKS.json %s (int8 = 2 x bf16 nominal)"
+                              % ("bf16_tflops_sustained" if sustained else "bf16_tflops"),
+                "algorithmic": {"modadds_per_step": modadds, "achieved_per_s": modadds / (kernel_ms_per_step / 1e3),
+                                "cuda_core_peak_per_s": alu_peak,
+                                "frac": modadds / (kernel_ms_per_step / 1e3) / alu_peak,
+                                "basis": "SURVEY 8(d.3) suffix-sum route (4 N^2 ell modular adds per shift) vs "
+                                         "148 SM x 64 ALU lanes x 1965 MHz / 5 lane-ops per 64-bit modular add; "
+                                         "> 1 means the int8 GEMM form beats any CUDA-core evaluation of it"}}
 
     def config(self):
         cfg = self.cfg
@@ -775,6 +789,7 @@ def main():
 
     if rank == 0:
         kms_step = k_ms / args.steps
+        W.timed_ms = ms
         roof = W.roofline(kms_step, ms_step)
         roof.update({"kernel_ms_per_step": kms_step, "kernel_launches": k_launches,
                      "kernel_share_of_step": kms_step / ms_step})
