@@ -164,8 +164,7 @@ FDFB_DEV void inv8_32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
 // final pass on positions 8 tid + k: P stages with pair distance t = 2^{P-1-s}; stage s
 // uses 8 >> (P - s) consecutive pairs of the thread's group
 template <int P, int V>
-FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
-  Tw8 t; load_tw8(t, g);
+FDFB_DEV void fwd_last32_t(u32 (&x)[V][8], const Tw8& t, u32 p, u32 p2, u32 z) {
   int o = 0;
 #pragma unroll
   for (int s = 0; s < P; s++) {
@@ -180,8 +179,20 @@ FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   }
 }
 template <int P, int V>
-FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
+FDFB_DEV void fwd_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
   Tw8 t; load_tw8(t, g);
+  fwd_last32_t<P, V>(x, t, p, p2, z);
+}
+// the thread's final-pass group held in TMEM (16 words: (w, w') pairs), see k_blind_rotate_p
+FDFB_DEV void load_tw8_tmem(Tw8& t, uint32_t taddr) {
+  u32 v[16];
+  tmem_ld16(taddr, v);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 8; i++) { t.w[i] = v[2 * i]; t.s[i] = v[2 * i + 1]; }
+}
+template <int P, int V>
+FDFB_DEV void inv_last32_t(u32 (&x)[V][8], const Tw8& t, u32 p, u32 p2, u32 z) {
   int o = 8 - (8 >> P);
 #pragma unroll
   for (int s = P - 1; s >= 0; s--) {
@@ -194,6 +205,11 @@ FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
         if ((k & d) == 0) bin32(x[v][k], x[v][k + d], t.w[o + (k >> (P - s))], t.s[o + (k >> (P - s))], p, p2, z);
     }
   }
+}
+template <int P, int V>
+FDFB_DEV void inv_last32(u32 (&x)[V][8], const uint4* g, u32 p, u32 p2, u32 z) {
+  Tw8 t; load_tw8(t, g);
+  inv_last32_t<P, V>(x, t, p, p2, z);
 }
 
 // Exchange-buffer layouts.  Exchange x (between radix-8 pass x and x+1) stores logical
@@ -556,9 +572,9 @@ FDFB_DEV void warp_arrive(uint32_t baddr) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(baddr) : "memory");
 }
-template <int N, int V>
+template <int N, int V, bool TWT>
 FDFB_DEV void fwd_consume(u32 (&x)[V][8], const u32* X, u32* sl, int tid, const uint4* tab, u32 p, u32 p2, u32 z,
-                          uint32_t empty_b) {
+                          uint32_t empty_b, uint32_t tw_taddr) {
   using S = BrShape<N>;
   constexpr int T1 = N >> 6;                       // pass-1 stride
   const int B = qbase<N, 1>(tid);
@@ -572,20 +588,28 @@ FDFB_DEV void fwd_consume(u32 (&x)[V][8], const u32* X, u32* sl, int tid, const 
   xload<N, S::NMID - 1, V>(x, sl, lay_base<N, S::NMID - 1>(8 * tid), 1);
   constexpr int BL = fwd_bound_before_last<N, 1, 8>();
   if constexpr (BL + 2 * S::PLAST > 16) red8p_all<V>(x, p2);
-#ifdef FDFB_EXP_TW
-  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + (tid & FDFB_EXP_TW)), p, p2, z);
-#else
-  fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
-#endif
+  if constexpr (TWT) {
+    Tw8 t;
+    load_tw8_tmem(t, tw_taddr);
+    fwd_last32_t<S::PLAST, V>(x, t, p, p2, z);
+  } else {
+    fwd_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+  }
 }
 // inverse up to the cross-warp store: last pass in registers, warp-local passes through the
 // slab, pass 1 -> layout 0 into X[b]
-template <int N, int V>
+template <int N, int V, bool TWT>
 FDFB_DEV void inv_produce(u32 (&x)[V][8], u32* X, u32* sl, int tid, const uint4* tab, u32 p, u32 p2, u32 z,
-                          uint32_t empty_b, uint32_t empty_par, uint32_t full_b) {
+                          uint32_t empty_b, uint32_t empty_par, uint32_t full_b, uint32_t tw_taddr) {
   using S = BrShape<N>;
   constexpr int NM = S::NMID;
-  inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+  if constexpr (TWT) {
+    Tw8 t;
+    load_tw8_tmem(t, tw_taddr);
+    inv_last32_t<S::PLAST, V>(x, t, p, p2, z);
+  } else {
+    inv_last32<S::PLAST, V>(x, tab + 4 * (S::G_LAST + tid), p, p2, z);
+  }
   __syncwarp();
   xstore<N, NM - 1, V>(x, sl, lay_base<N, NM - 1>(8 * tid), 1);
   __syncwarp();
@@ -636,7 +660,12 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   if (tid == 0) {
     for (int b = 0; b < 2 * BR_NB; b++) mbar_init(bars + b, T / 32);   // one arrival per warp
   }
-  constexpr int TCOLS = T > 128 ? 64 : 32;         // 32 words per thread; warps w, w + 4 share lanes
+  // TMEM per warp group (warps w and w + 4 share TMEM lanes): 32 columns of d, and for N = 2048
+  // (TWT) the thread's final-pass twiddle groups of every prime and direction (16 words each)
+  constexpr bool TWT = (N == 2048);
+  constexpr int GCOLS = TWT ? 128 : 32;
+  constexpr int TCOLS = T > 128 ? 2 * GCOLS : GCOLS;
+  static_assert(!TWT || 32 + 16 * 2 * NP <= GCOLS, "twiddle columns");
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)),
                  "n"(TCOLS));
@@ -646,7 +675,21 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   __syncthreads();
   tc_fence_after();
   // this thread's 32 TMEM words: lanes 32 (warp % 4) .., column group warp / 4
-  const uint32_t tm = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+  const uint32_t tm = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(GCOLS * (warp >> 2));
+  if constexpr (TWT) {                             // stage the final-pass twiddles once per CTA
+#pragma unroll 1
+    for (int q = 0; q < 2 * NP; q++) {
+      const uint4* g = (q & 1 ? R.itab : R.ftab) + ((size_t)(q >> 1) * S::GROUPS + S::G_LAST + tid) * 4;
+      u32 v[16];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const uint4 a = __ldg(g + i);
+        v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
+      }
+      tmem_st16(tm + 32 + 16 * q, v);
+    }
+    tmem_st_wait();
+  }
   const uint32_t bar0 = smem_u32(bars);            // full[b] = bar0 + 8 b, empty[b] = bar0 + 8 NB + 8 b
   constexpr uint32_t EO = 8 * BR_NB;
   int cpb = 0, ccb = 0;                            // buffer of the next produced / consumed transform
@@ -738,7 +781,8 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
           const int b = ccb;
           mbar_wait_sleep(bar0 + 8 * b, ccp);
           const uint4* ft = R.ftab + (size_t)pi * S::GROUPS * 4;
-          fwd_consume<N, 2>(x, Xb + b * 2 * W, sl, tid, ft, R.p[pi], R.p2[pi], R.zero, bar0 + EO + 8 * b);
+          fwd_consume<N, 2, TWT>(x, Xb + b * 2 * W, sl, tid, ft, R.p[pi], R.p2[pi], R.zero, bar0 + EO + 8 * b,
+                                 tm + 32 + 32 * pi);
           if (++ccb == BR_NB) { ccb = 0; ccp ^= 1; }
 #pragma unroll
           for (int v = 0; v < 2; v++) {
@@ -761,8 +805,8 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
           for (int k = 0; k < 8; k++) { x[0][k] = redc64(mb[k], R, pi); x[1][k] = redc64(ma[k], R, pi); }
           const int b = cpb;
           const uint4* it = R.itab + (size_t)pi * S::GROUPS * 4;
-          inv_produce<N, 2>(x, Xb + b * 2 * W, sl, tid, it, R.p[pi], R.p2[pi], R.zero, bar0 + EO + 8 * b, cpp ^ 1,
-                            bar0 + 8 * b);
+          inv_produce<N, 2, TWT>(x, Xb + b * 2 * W, sl, tid, it, R.p[pi], R.p2[pi], R.zero, bar0 + EO + 8 * b,
+                                 cpp ^ 1, bar0 + 8 * b, tm + 32 + 32 * pi + 16);
           if (++cpb == BR_NB) { cpb = 0; cpp ^= 1; }
         };
         auto consume_inv = [&](int pi) {
