@@ -566,6 +566,11 @@ k_blind_rotate(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __res
 // (86 KB at N = 2048; 2 CTAs per SM as before).  Per CMux:
 //   P(F0) P(F1) C(F0) P(F2) C(F1) P(F3) C(F2) C(F3) P(I) P(F0') C(I) P(F1') C(F0') ...
 // (F: forward digit-pair transforms of a prime, I: its inverse; ' = next prime).
+// brK loads of the pipelined kernel: __ldg after an L1 prefetch at the start of the consume
+// (measured per 296-accumulator wave: 91.9 ms; L1::no_allocate loads 103.1 ms without a
+// prefetch, 95.3 ms with an L2 prefetch -- the L1 prefetch hides the latency)
+FDFB_DEV uint4 ld_key(const uint4* p) { return __ldg(p); }
+FDFB_DEV void prefetch_key(const u32* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 // one arrival per warp: __syncwarp orders the lanes' shared-memory accesses before lane 0's
 // (release) arrive, so the barriers count warps, not threads
 FDFB_DEV void warp_arrive(uint32_t baddr) {
@@ -772,11 +777,11 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
           const u32* K = Kstep + (size_t)pi * prime_words;
           const u32* Kb0 = K + (size_t)((half * ell + r) * 2) * N;
           const u32* Kb1 = Kb0 + 2 * N;
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb0));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb0 + N));
+          prefetch_key(Kb0);
+          prefetch_key(Kb0 + N);
           if (two) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Kb1 + N));
+            prefetch_key(Kb1);
+            prefetch_key(Kb1 + N);
           }
           const int b = ccb;
           mbar_wait_sleep(bar0 + 8 * b, ccp);
@@ -789,8 +794,8 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
             if (v == 1 && !two) break;
             const u32* Kb = v ? Kb1 : Kb0;
             const u32* Ka = Kb + N;
-            const uint4 kb0 = __ldg((const uint4*)Kb), kb1 = __ldg((const uint4*)Kb + 1);
-            const uint4 ka0 = __ldg((const uint4*)Ka), ka1 = __ldg((const uint4*)Ka + 1);
+            const uint4 kb0 = ld_key((const uint4*)Kb), kb1 = ld_key((const uint4*)Kb + 1);
+            const uint4 ka0 = ld_key((const uint4*)Ka), ka1 = ld_key((const uint4*)Ka + 1);
             const u32 kb[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
             const u32 ka[8] = {ka0.x, ka0.y, ka0.z, ka0.w, ka1.x, ka1.y, ka1.z, ka1.w};
 #pragma unroll
