@@ -252,7 +252,7 @@ static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, 
     cudaGetLastError();
     if (getenv("FDFB_DEBUG")) fprintf(stderr, "k_blind_rotate_p<%d,%d,%d>: %d CTAs per SM\n", N, NP, (int)GIN, per_sm);
     if (per_sm < 1) per_sm = 1;
-    const int tmem_cap = 512 / (N == 2048 ? 256 : (T > 128 ? 64 : 32));   // TMEM columns per CTA
+    const int tmem_cap = 512 / ((N >= 1024 ? 128 : 32) * (T > 128 ? 2 : 1));   // TMEM columns per CTA
     if (per_sm > tmem_cap) per_sm = tmem_cap;
     int grid = c->num_sms * per_sm;
     if (grid > n_acc) grid = n_acc;

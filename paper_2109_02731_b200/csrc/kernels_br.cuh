@@ -667,7 +667,7 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   }
   // TMEM per warp group (warps w and w + 4 share TMEM lanes): 32 columns of d, and for N = 2048
   // (TWT) the thread's final-pass twiddle groups of every prime and direction (16 words each)
-  constexpr bool TWT = (N == 2048);
+  constexpr bool TWT = (N >= 1024);               // 128 columns per warp group: fits MINB CTAs per SM
   constexpr int GCOLS = TWT ? 128 : 32;
   constexpr int TCOLS = T > 128 ? 2 * GCOLS : GCOLS;
   static_assert(!TWT || 32 + 16 * 2 * NP <= GCOLS, "twiddle columns");
