@@ -42,9 +42,14 @@ IMAD_PER_MODMUL = 16
 
 
 def imad_per_modmul(cfg):
-    """Slots of one direct lazy Shoup modmul at the configuration's word size: 16 for a 54-bit
-    Q (above), 4 for Q < 2^32 (IMAD.HI + 2 IMAD on 32-bit words)."""
-    return IMAD_PER_MODMUL if cfg["Q"] >= (1 << 32) else 4
+    """Slots of the cheapest direct Shoup modmul at the configuration's modulus width:
+    - Q < 2^31: 4 (IMAD.HI + 2 IMAD on 32-bit words; the result in [0, 2Q) fits 32 bits);
+    - 2^31 <= Q < 2^32 (FHEW-like, Q = 2^32 - 10239): 6 -- [0, 2Q) no longer fits a 32-bit word,
+      so a*w - q*Q is formed in 64 bits: IMAD.HI + 2 IMAD.WIDE (2 slots each);
+    - otherwise 16 (the 54-bit Shoup above)."""
+    if cfg["Q"] < (1 << 31):
+        return 4
+    return 6 if cfg["Q"] < (1 << 32) else IMAD_PER_MODMUL
 # DRAM traffic of one bench step, measured: `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum`
 # over every launch of one step of this workload (tools/traffic_step.py; the summary JSON is
 # committed under profiles/<round>/traffic_<workload>.json and read at run time).  None if absent.
@@ -314,7 +319,7 @@ class BootstrapWorkload:
                 "modmul_per_step": modmul_step, "imad_per_modmul": imad_per_modmul(self.cfg),
                 "modmul_per_s": modmul_step / (kernel_ms_per_step / 1e3),
                 "peak_basis": "fmaheavy pipe: 148 SM x 64 IMAD slots/clk x 1965 MHz; "
-                              "16 slots per 54-bit Shoup modmul (4 for Q < 2^32)"}
+                              "16 slots per 54-bit Shoup modmul (6 for 2^31 <= Q < 2^32, 4 for Q < 2^31)"}
 
     def config(self):
         return bootstrap_config(self.cfg, self.B, self.world, self.box)

@@ -45,7 +45,15 @@ struct fdfb_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   mutable std::mutex boot_mu;             // serialises the fork/join enqueue of concurrent callers
   int imma_wide_k = 65536;   // FDFB_IMMA_WIDE_K: K from which pair tiles are 448 columns wide
+  // key-stream pacing of k_blind_rotate_p (kernels_br.cuh pace_wait): FDFB_BR_PACE = "wlo,whi" in
+  // steps, "0" off; one position slot per CTA in one of BR_PACE_SLOTS per-launch regions
+  u32 br_wlo = 32, br_whi = 160, br_wcap = 8;     // cap: at most 8 sleeps of ~2 us per check
+  bool br_pace_split = true;              // FDFB_BR_PACE_SPLIT=0: do not pace the two-part bootstrap's halves
+  u64* d_prog = nullptr;                  // [BR_PACE_SLOTS][BR_PACE_MAXGRID], allocated at ctx_create
+  mutable std::atomic<u32> br_tag{0};
 };
+#define BR_PACE_SLOTS 16
+#define BR_PACE_MAXGRID 4096
 
 // Bracket one launch of kernel class `cls` with events on its stream when timing is on.
 struct TimedLaunch {
@@ -229,7 +237,7 @@ static int launch_br_small(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_a
 
 template <int N, int NP, bool GIN>
 static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, int acc_per_ct, int abar_rows,
-                       const u32* abar, const u64* gin, int s_begin, cudaStream_t st) {
+                       const u32* abar, const u64* gin, int s_begin, cudaStream_t st, bool pace) {
   constexpr int T = N / 8;
   if (c->br_kernel != 1) {                     // pipelined kernel (mbarrier-decoupled exchanges, d in TMEM)
     const size_t sm = (25 + 9 * BR_NB) * (size_t)N;   // acc 16N + NB cross-warp buffers 9N each + slabs 9N
@@ -256,9 +264,17 @@ static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, 
     if (per_sm > tmem_cap) per_sm = tmem_cap;
     int grid = c->num_sms * per_sm;
     if (grid > n_acc) grid = n_acc;
+    // pacing (kernels_br.cuh pace_wait): only where a CTA processes more than one accumulator
+    u32 tag = 0, wlo = 0, whi = 0, wcap = 0;
+    u64* prog = nullptr;
+    if (!GIN && pace && c->br_wlo && grid <= BR_PACE_MAXGRID && n_acc > grid) {
+      do tag = ++c->br_tag; while (tag == 0);
+      prog = c->d_prog + (size_t)(tag % BR_PACE_SLOTS) * BR_PACE_MAXGRID;
+      wlo = c->br_wlo; whi = c->br_whi; wcap = c->br_wcap;
+    }
     TimedLaunch tl(c, FDFB_KCLASS_BLIND_ROTATE, st);
     k_blind_rotate_p<N, NP, GIN><<<grid, T, sm, st>>>(c->dp, c->rns, bsk, accs, n_acc, acc_per_ct, abar_rows, abar,
-                                                       gin, s_begin);
+                                                       gin, s_begin, prog, tag, wlo, whi, wcap);
     CKL(c);
     return FDFB_OK;
   }
@@ -279,7 +295,7 @@ static int launch_br_t(const fdfb_ctx* c, const u32* bsk, u64* accs, int n_acc, 
 // blind-rotate n_acc accumulators; accumulator g uses mask row (g / acc_per_ct) % abar_rows
 // gin != nullptr: one shift-based step s_begin (k_blind_rotate GIN mode), else steps [0, n u)
 static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, int acc_per_ct, const u32* abar,
-                     cudaStream_t st, int abar_rows = 0, const u64* gin = nullptr, int s_begin = 0) {
+                     cudaStream_t st, int abar_rows = 0, const u64* gin = nullptr, int s_begin = 0, bool pace = true) {
   if (n_acc <= 0) return FDFB_OK;
   if (abar_rows <= 0) abar_rows = (n_acc + acc_per_ct - 1) / acc_per_ct;
   const u32* k = (const u32*)bsk;
@@ -308,12 +324,12 @@ static int launch_br(const fdfb_ctx* c, const u64* bsk, u64* accs, int n_acc, in
 #define BR_CASE(NN)                                                                                          \
   case NN:                                                                                                   \
     if (gin)                                                                                                 \
-      return np == 3 ? launch_br_t<NN, 3, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st) \
-           : np == 2 ? launch_br_t<NN, 2, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st) \
-                     : launch_br_t<NN, 1, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st); \
-    return np == 3 ? launch_br_t<NN, 3, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st)  \
-         : np == 2 ? launch_br_t<NN, 2, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st)  \
-                   : launch_br_t<NN, 1, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st);
+      return np == 3 ? launch_br_t<NN, 3, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st, pace) \
+           : np == 2 ? launch_br_t<NN, 2, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st, pace) \
+                     : launch_br_t<NN, 1, true>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st, pace); \
+    return np == 3 ? launch_br_t<NN, 3, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st, pace)  \
+         : np == 2 ? launch_br_t<NN, 2, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st, pace)  \
+                   : launch_br_t<NN, 1, false>(c, k, accs, n_acc, acc_per_ct, abar_rows, abar, gin, s0, st, pace);
   switch (c->prm.N) {
     BR_CASE(256)
     BR_CASE(512)
@@ -662,6 +678,15 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   CK(cudaMalloc(&c->d_tables, ntab * sizeof(u64)));
   CK(cudaMalloc(&c->d_status, sizeof(int)));
   CK(cudaMemset(c->d_status, 0, sizeof(int)));
+  CK(cudaMalloc(&c->d_prog, (size_t)BR_PACE_SLOTS * BR_PACE_MAXGRID * sizeof(u64)));
+  CK(cudaMemset(c->d_prog, 0, (size_t)BR_PACE_SLOTS * BR_PACE_MAXGRID * sizeof(u64)));
+  if (const char* e = getenv("FDFB_BR_PACE_SPLIT")) c->br_pace_split = atoi(e) != 0;
+  if (const char* e = getenv("FDFB_BR_PACE")) {
+    unsigned lo = 0, hi = 0, cap = 0;
+    const int nf = sscanf(e, "%u,%u,%u", &lo, &hi, &cap);
+    if (nf >= 2 && lo > 0 && hi > lo) { c->br_wlo = lo; c->br_whi = hi; if (nf == 3) c->br_wcap = cap; }
+    else c->br_wlo = c->br_whi = 0;
+  }
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
   if ((rc = setup_rns(c))) { delete c; return rc; }
   if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
@@ -713,6 +738,7 @@ extern "C" void fdfb_ctx_destroy(fdfb_ctx* c) {
   }
   cudaFree(c->d_tables);
   cudaFree(c->d_status);
+  cudaFree(c->d_prog);
   cudaFree(c->d_rtab);
   if (c->helper) cudaStreamDestroy(c->helper);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -1117,7 +1143,7 @@ static int keyswitch_lwe(const fdfb_ctx* c, const u64* ksk, const u64* lwe, int 
 // BuildAcc, the final rotation, extraction and the LWE key switch, on stream st.
 static int boot_part(const fdfb_ctx* c, const void* brk, const void* bpk, const void* ksk, const uint64_t* rotp,
                      uint32_t k, uint64_t* ct_out, uint32_t B, const BootWs& w, uint32_t s0, uint32_t cnt,
-                     void* ks_ws, cudaStream_t st) {
+                     void* ks_ws, cudaStream_t st, bool pace) {
   const fdfb_params& p = c->prm;
   const int N = p.N, ellb = p.ell_boot;
   if (cnt == 0) return FDFB_OK;
@@ -1129,7 +1155,7 @@ static int boot_part(const fdfb_ctx* c, const void* brk, const void* bpk, const 
   const u32* abar = w.abar + (size_t)s0 * p.n;
   const u32* bbar = w.bbar + s0;
   // 3. ell_boot blind rotations of every ciphertext, batched
-  if ((rc = launch_br(c, (const u64*)brk, accs, (int)(cnt * ellb), ellb, abar, st))) return rc;
+  if ((rc = launch_br(c, (const u64*)brk, accs, (int)(cnt * ellb), ellb, abar, st, 0, nullptr, 0, pace))) return rc;
   // 4. SampleExt(., 1) + L^{i-1}/2
   tot = (size_t)cnt * ellb * (N + 1);
   k_ladder_extract<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, accs, (int)(cnt * ellb), lad);
@@ -1157,7 +1183,7 @@ static int boot_part(const fdfb_ctx* c, const void* brk, const void* bpk, const 
   for (uint32_t kk = 0; kk < k; kk++) {
     u64* F = w.F + ((size_t)kk * B + s0) * 2 * N;
     u64* o = w.lweN + ((size_t)ellb * B + (size_t)kk * B + s0) * (N + 1);
-    if ((rc = launch_br(c, (const u64*)brk, F, (int)cnt, 1, abar, st, (int)cnt))) return rc;
+    if ((rc = launch_br(c, (const u64*)brk, F, (int)cnt, 1, abar, st, (int)cnt, nullptr, 0, pace))) return rc;
     tot = (size_t)cnt * (N + 1);
     k_extract_modswitch<<<grid_for(tot, 256, c->num_sms), 256, 0, st>>>(c->dp, F, (int)cnt, o);
     CKL(c);
@@ -1192,13 +1218,13 @@ static int bootstrap_impl(const fdfb_ctx* c, const void* brk, const void* bpk, c
   void* ks0 = w.ks;
   void* ks1 = (char*)w.ks + w.ks_part;
   const bool split = c->boot_split && k == 1 && B >= 64;
-  if (!split) return boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, 0, B, ks0, st);
+  if (!split) return boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, 0, B, ks0, st, true);
   const uint32_t h = B / 2;
   std::lock_guard<std::mutex> lock(c->boot_mu);
   CK(cudaEventRecord(c->ev_fork, st));
   CK(cudaStreamWaitEvent(c->helper, c->ev_fork, 0));
-  int rc = boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, 0, h, ks0, st);
-  int rc2 = boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, h, B - h, ks1, c->helper);
+  int rc = boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, 0, h, ks0, st, c->br_pace_split);
+  int rc2 = boot_part(c, brk, bpk, ksk, rotp, k, ct_out, B, w, h, B - h, ks1, c->helper, c->br_pace_split);
   CK(cudaEventRecord(c->ev_join, c->helper));
   CK(cudaStreamWaitEvent(st, c->ev_join, 0));
   return rc ? rc : rc2;

@@ -628,6 +628,46 @@ FDFB_DEV void inv_produce(u32 (&x)[V][8], u32* X, u32* sl, int tid, const uint4*
   warp_arrive(full_b);
 }
 
+// Key-stream pacing of the persistent batched kernel.  brK is read once per step by every
+// resident accumulator; the CTAs of a launch only share those reads through L2 while they are
+// at nearby steps.  Free-running CTAs drift apart over the ~35 accumulators each processes (a
+// key step is 393 KB at the Large set, so L2 holds ~300 steps), and then every CTA streams brK
+// from HBM on its own.  Every BR_PACE_CH steps warp 0 publishes the CTA's position
+// pos = round * n u + step (tagged with the launch's tag) to prog[blockIdx.x] and waits while
+// any CTA of the launch is between wlo and whi steps behind it.  CTAs further behind (late
+// starters of a launch that shares the GPU with another one) are ignored, finished CTAs publish
+// tag 0.  A wait lasts at most `cap` polls of ~2 us, so CTAs that are faster for a structural
+// reason (an SM shared with fewer CTAs) lose a bounded fraction of their time while the small
+// steady-state drift is still corrected; CTAs in their first or last round (staggered starts,
+// partners leaving) publish but never wait.  The CTA furthest behind never waits, so the launch
+// always progresses; the pacing changes no arithmetic.
+#ifndef BR_PACE_CH
+#define BR_PACE_CH 8
+#endif
+FDFB_DEV void pace_publish(u64* prog, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(prog), "l"(v) : "memory");
+}
+FDFB_DEV u64 pace_load(const u64* prog) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(prog) : "memory");
+  return v;
+}
+FDFB_DEV void pace_wait(u64* prog, u32 tag, u32 pos, u32 wlo, u32 whi, u32 cap) {   // all lanes of one warp
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) pace_publish(prog + blockIdx.x, ((u64)tag << 32) | pos);
+  if (cap == 0) return;                            // publish only
+  for (u32 it = 0;; it++) {
+    bool behind = false;
+    for (int c = lane; c < (int)gridDim.x; c += 32) {
+      const u64 v = pace_load(prog + c);
+      const u32 q = (u32)v;
+      if ((u32)(v >> 32) == tag && q + wlo <= pos && q + whi > pos) behind = true;   // pos - whi < q <= pos - wlo
+    }
+    if (!__any_sync(0xffffffffu, behind) || it == cap) break;   // at most cap sleeps
+    __nanosleep(2000);
+  }
+}
+
 #ifndef BR_NB
 #define BR_NB 3      // cross-warp exchange buffers of k_blind_rotate_p
 #endif
@@ -638,7 +678,7 @@ template <int N, int NP, bool GIN>
 __global__ void __launch_bounds__(N / 8, BrShape<N>::MINB)
 k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __restrict__ accs, int n_acc,
                  int acc_per_ct, int abar_rows, const u32* __restrict__ abar, const u64* __restrict__ gin,
-                 int s_begin) {
+                 int s_begin, u64* __restrict__ prog, u32 tag, u32 wlo, u32 whi, u32 wcap) {
   using S = BrShape<N>;
   constexpr int T = S::T;
   constexpr int W = Lay<N>::WORDS;
@@ -701,8 +741,9 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   uint32_t cpp = 0, ccp = 0;                       // and its use parity (flips when the buffer index wraps)
   u32 x[2][8];
   u64 mb[8], ma[8];
+  u32 pos0 = 0;                                    // pacing position of this round's step 0
 
-  for (int g = blockIdx.x; g < n_acc; g += gridDim.x) {
+  for (int g = blockIdx.x; g < n_acc; g += gridDim.x, pos0 += (u32)(p.n * u)) {
     u64* acc = accs + (size_t)g * 2 * N;
     __syncthreads();
 #pragma unroll
@@ -724,6 +765,11 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
 #else
         const u32* Kstep = bsk + ((size_t)i * u + j) * step_words + 8 * tid;
 #endif
+        if constexpr (!GIN) {                      // pacing: publish always, wait only in middle rounds
+          const u32 s = (u32)(i * u + j);
+          if (wlo && warp == 0 && (s % BR_PACE_CH) == 0)
+            pace_wait(prog, tag, pos0 + s, wlo, whi, (pos0 > 0 && g + (int)gridDim.x < n_acc) ? wcap : 0u);
+        }
         __syncthreads();                           // acc of the previous step complete
         {                                          // d = acc X^e - acc (both halves) -> TMEM
           u32 dw[16];
@@ -881,6 +927,7 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
 #pragma unroll
     for (int k = 0; k < 16; k++) acc[tid + T * k] = sacc[tid + T * k];
   }
+  if (!GIN && wlo && tid == 0) pace_publish(prog + blockIdx.x, 0);   // finished: nobody waits on this CTA
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

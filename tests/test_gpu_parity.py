@@ -774,3 +774,57 @@ def test_bootstrap_two_part_split_equals_one_part_and_oracle(monkeypatch):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ctx.bootstrap_batch(dk, rot, T(other)))
+
+
+@pytest.mark.parametrize("pace", ["0", "8,4096,1000000", "32,160"])
+def test_blind_rotate_key_pacing_changes_no_bytes(pace, monkeypatch):
+    """Key-stream pacing of the persistent kernel (kernels_br.cuh pace_wait) only delays CTAs:
+    with more accumulators than resident CTAs (several rounds per CTA) the bytes equal the
+    oracle-checked unpaced run, also with a tight window that makes CTAs wait all the time."""
+    cfg, orc, K, ctx, dk = setup("tiny")
+    monkeypatch.setenv("FDFB_BR_CLUSTER", "0")
+    g = torch.Generator(device="cuda").manual_seed(77)
+    n_acc = 6000                                                 # > 148 x 16 resident CTAs at N = 256
+    acc = torch.randint(0, cfg["Q"], (n_acc, 2, cfg["N"]), device="cuda", generator=g).to(torch.uint64)
+    abar = torch.randint(0, 2 * cfg["N"], (n_acc, cfg["n"]), device="cuda", generator=g).to(torch.uint32)
+    monkeypatch.setenv("FDFB_BR_PACE", "0")
+    ref = H(Context(cfg, 0).blind_rotate(dk["brk"], acc.clone(), abar))
+    monkeypatch.setenv("FDFB_BR_PACE", pace)
+    got = H(Context(cfg, 0).blind_rotate(dk["brk"], acc.clone(), abar))
+    assert np.array_equal(got, ref)
+    A, ab = H(acc), H(abar)
+    for i in (0, 2367, 5999):
+        assert np.array_equal(got[i], orc.blind_rotate(K["brk"], A[i], ab[i]))
+
+
+# ADVICE r1 (medium): the int8 key-switch GEMMs split each centred key coefficient into 7 balanced
+# base-256 digits, exact for |v| <= 2^54, so validate() accepts Q < 2^55 and q_lwe <= 2^55.  This
+# set sits at both limits: Q the largest prime below 2^55 with Q = 1 mod 2N, q_lwe = 2^55.
+EDGE = dict(synth.load_config("tiny"), name="edge", Q=36028797018963457, log_q_lwe=55,
+            logL_rgsw=14, ell_rgsw=4, logL_boot=11, ell_boot=5, logL_pk=14, ell_pk=4, logL_ks=5, ell_ks=11,
+            logL_pack=12, ell_pack=5)
+
+
+def test_edge_moduli_keyswitch_and_bootstrap_bit_exact():
+    cfg = EDGE
+    orc = Oracle(cfg)
+    K = orc.keys(cfg["seeds"]["keys"])
+    ctx = Context(cfg, 0)
+    dk = {"brk": ctx.key_import(KEY_BRK, T(K["brk"].reshape(-1))),
+          "bpk": ctx.key_import(KEY_BPK, T(K["bpk"].reshape(-1))),
+          "ksk": ctx.key_import(KEY_KSK, T(K["ksk"].reshape(-1)))}
+    ksk = K["ksk"].astype(object) % (1 << 55)
+    cen = np.where(ksk >= (1 << 54), ksk - (1 << 55), ksk)
+    assert int(np.abs(cen).max()) > (1 << 54) - (1 << 48)            # key coefficients at the digit limit
+    rng = np.random.default_rng(11)
+    c = rng.integers(0, 1 << 55, (21, cfg["N"] + 1), dtype=np.uint64)
+    c[0, :] = (1 << 55) - 1                                         # every digit at its maximum
+    got = H(ctx.lwe_keyswitch(dk["ksk"], T(c)))
+    for i in range(21):
+        assert np.array_equal(got[i], orc.keyswitch_lwe(K["ksk"], c[i])), i
+    assert np.array_equal(H(ctx.lwe_keyswitch(dk["ksk"], T(c), gemm=False)), got)
+    f = synth.lut(cfg, seed=12)
+    rotp = orc.setup_polynomial(orc.bootsmap(f))
+    cts = orc.lwe_encrypt(13, K["s"], synth.messages(cfg, 6, seed=14))
+    got = H(ctx.bootstrap_batch(dk, ctx.setup_lut(f), T(cts)))     # BuildAcc switch with pK mod Q ~ 2^55
+    assert np.array_equal(got, orc.bootstrap(K, rotp, cts))

@@ -34,15 +34,18 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("name,total", [("tiny", 37), ("large", 2 * 296 + 37)])
-def test_sharded_bootstrap_equals_single_rank_bytes(name, total, tmp_path):
+@pytest.mark.parametrize("name,total,backend,world", [("tiny", 37, "gloo", 2), ("large", 2 * 296 + 37, "gloo", 2),
+                                                     ("tiny", 37, "nccl", 1)])
+def test_sharded_bootstrap_equals_single_rank_bytes(name, total, backend, world, tmp_path):
+    """gloo: two ranks share the GPU.  nccl: the key broadcast and output all-gather go through
+    NCCL on device tensors (a world of one rank: one GPU per rank, and the box has one)."""
     here = os.path.dirname(os.path.abspath(__file__))
     port = _free_port()
     out_path = str(tmp_path / "sharded.npz")
     procs = []
-    for r in range(2):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
-                   FDFB_SHARE_DEVICE="1")
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   FDFB_SHARE_DEVICE="1", FDFB_TEST_BACKEND=backend)
         procs.append(subprocess.Popen([sys.executable, os.path.join(here, "sharded_worker.py"), name, str(total),
                                        out_path], env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
     outs = [p.communicate(timeout=900) for p in procs]
