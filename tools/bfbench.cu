@@ -92,6 +92,42 @@ __global__ void k_bf_i2f(uint32_t* out, uint32_t p, uint32_t w0, double wd0, lon
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// mixed: NF of the CH chains take the FP64 quotient (fp64 pipe), the others the Shoup IMAD.HI
+// (multiply pipe): the two pipes run in parallel
+template <int NF>
+__global__ void k_bf_mix(uint32_t* out, uint32_t p, uint32_t w0, uint32_t ws0, double wd0, long long* cyc) {
+  uint32_t x[CH], y[CH];
+  for (int c = 0; c < CH; c++) { x[c] = (threadIdx.x * 977 + c * 131) % p; y[c] = (threadIdx.x * 613 + c * 71) % p; }
+  const uint32_t p2 = 2 * p;
+  const uint32_t w = w0 + (threadIdx.x & 1), ws = ws0 + (threadIdx.x & 1);
+  const double wd = wd0 * (1.0 + 1e-12 * (threadIdx.x & 1));
+  const double M = 4503599627370496.0, R = 6755399441055744.0;
+  long long t0 = clock64();
+#pragma unroll 2
+  for (int i = 0; i < IT; i++) {
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+      uint32_t t;
+      if (c < NF) {
+        const double yd = __hiloint2double(0x43300000, (int)y[c]) - M;
+        const uint32_t q = (uint32_t)__double2loint(fma(yd, wd, R));
+        t = y[c] * w - q * p + p;
+      } else {
+        const uint32_t q = __umulhi(y[c], ws);
+        t = y[c] * w - q * p;
+      }
+      const uint32_t nx = x[c] + t, ny = x[c] - t + p2;
+      x[c] = csub(nx, p2);
+      y[c] = csub(ny, p2);
+    }
+  }
+  long long t1 = clock64();
+  uint32_t r = 0;
+  for (int c = 0; c < CH; c++) r ^= x[c] ^ y[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 // correctness of the FP64 quotient over many (y, w): t must land in (0, 2p) and equal y w mod p
 __global__ void k_check(uint32_t p, uint32_t* bad, unsigned long long n) {
   for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
@@ -127,7 +163,7 @@ int main() {
   cudaMemcpy(&hbad, bad, 4, cudaMemcpyDeviceToHost);
   printf("{\"fp64_quotient_check\": {\"samples\": %llu, \"bad\": %u}}\n", 1ull << 30, hbad);
   for (int blocks_per_sm = 2; blocks_per_sm <= 8; blocks_per_sm *= 2) {
-    for (int v = 0; v < 3; v++) {
+    for (int v = 0; v < 7; v++) {
       const int grid = sms * blocks_per_sm;
       cudaEvent_t a, b;
       cudaEventCreate(&a); cudaEventCreate(&b);
@@ -135,7 +171,11 @@ int main() {
         cudaEventRecord(a);
         if (v == 0) k_bf_shoup<<<grid, TPB>>>(out, p, w, ws, cyc);
         else if (v == 1) k_bf_fp64<<<grid, TPB>>>(out, p, w, wd, cyc);
-        else k_bf_i2f<<<grid, TPB>>>(out, p, w, wd, cyc);
+        else if (v == 2) k_bf_i2f<<<grid, TPB>>>(out, p, w, wd, cyc);
+        else if (v == 3) k_bf_mix<1><<<grid, TPB>>>(out, p, w, ws, wd, cyc);
+        else if (v == 4) k_bf_mix<2><<<grid, TPB>>>(out, p, w, ws, wd, cyc);
+        else if (v == 5) k_bf_mix<3><<<grid, TPB>>>(out, p, w, ws, wd, cyc);
+        else k_bf_mix<4><<<grid, TPB>>>(out, p, w, ws, wd, cyc);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
       }
@@ -144,7 +184,7 @@ int main() {
       const double bfly = (double)grid * TPB * CH * IT;
       const double per_sm_clk = bfly / (ms * 1e-3) / sms / (clk * 1e3);
       printf("{\"variant\": \"%s\", \"blocks_per_sm\": %d, \"ms\": %.3f, \"butterflies_per_sm_per_clk_nominal\": %.2f, "
-             "\"err\": \"%s\"}\n", v == 0 ? "shoup" : (v == 1 ? "fp64_magic" : "fp64_i2f"), blocks_per_sm, ms,
+             "\"err\": \"%s\"}\n", (const char*[]){"shoup", "fp64_magic", "fp64_i2f", "mix1of8", "mix2of8", "mix3of8", "mix4of8"}[v], blocks_per_sm, ms,
              per_sm_clk, cudaGetErrorString(cudaGetLastError()));
     }
   }
