@@ -741,9 +741,8 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
   uint32_t cpp = 0, ccp = 0;                       // and its use parity (flips when the buffer index wraps)
   u32 x[2][8];
   u64 mb[8], ma[8];
-  u32 pos0 = 0;                                    // pacing position of this round's step 0
 
-  for (int g = blockIdx.x; g < n_acc; g += gridDim.x, pos0 += (u32)(p.n * u)) {
+  for (int g = blockIdx.x; g < n_acc; g += gridDim.x) {
     u64* acc = accs + (size_t)g * 2 * N;
     __syncthreads();
 #pragma unroll
@@ -767,8 +766,11 @@ k_blind_rotate_p(DevParams p, RnsParams R, const u32* __restrict__ bsk, u64* __r
 #endif
         if constexpr (!GIN) {                      // pacing: publish always, wait only in middle rounds
           const u32 s = (u32)(i * u + j);
-          if (wlo && warp == 0 && (s % BR_PACE_CH) == 0)
-            pace_wait(prog, tag, pos0 + s, wlo, whi, (pos0 > 0 && g + (int)gridDim.x < n_acc) ? wcap : 0u);
+          if (wlo && warp == 0 && (s % BR_PACE_CH) == 0) {   // everything derived here: no loop-carried state
+            const u32 rnd = (u32)(g - (int)blockIdx.x) / gridDim.x;
+            const bool mid = rnd > 0 && g + (int)gridDim.x < n_acc;
+            pace_wait(prog, tag, rnd * (u32)(p.n * u) + s, wlo, whi, mid ? wcap : 0u);
+          }
         }
         __syncthreads();                           // acc of the previous step complete
         {                                          // d = acc X^e - acc (both halves) -> TMEM
