@@ -1,0 +1,9 @@
+#!/bin/bash
+# gpurun: verify HEAD -- full GPU suite, smoke, default bench line (and the bench's reference arm)
+cd "$(dirname "$0")/.."
+O=gpurun_out/head; mkdir -p $O
+timeout 2400 python -m pytest tests -m gpu -q -x --durations=10 > $O/pytest_gpu_all.log 2>&1; echo "rc=$?" >> $O/pytest_gpu_all.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+timeout 900 python bench.py > $O/bench_full.log 2>&1; echo "rc=$?" >> $O/bench_full.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > $O/bench_ref.log 2>&1; echo "rc=$?" >> $O/bench_ref.log
+echo done
