@@ -246,6 +246,11 @@ class BootstrapWorkload:
         import synth
         from paper_2109_02731_b200.dist import broadcast_keys, shard_range
         self.ctx, self.cfg, self.B, self.stream = ctx, cfg, B, stream
+        # labels follow the configuration (the class strings name the Large set the metric is quoted on);
+        # RNS primes of the blind rotation: Q itself below 2^28, else 2 (32-bit Q) or 3 (54-bit Q) primes
+        npr = 1 if cfg["Q"] < (1 << 28) else (2 if cfg["Q"] < (1 << 32) else 3)
+        self.metric = self.metric.replace("N=2048", "N=%d" % cfg["N"])
+        self.kernel = "k_blind_rotate_p<%d,%d>" % (cfg["N"], npr)
         t0 = time.perf_counter()
         if rank == 0:
             keys = ctx.keygen(cfg["seeds"]["keys"], which=0x0F)

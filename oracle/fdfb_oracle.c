@@ -589,15 +589,24 @@ void or_pack(const u64* P, const u64* pack, const u64* c, int d, u64* out) {
   free(s);
 }
 /* VectorPack(v, pK) = sum_{k=1}^{m} Pack(v[k], pK, k). */
+/* Schedule only: when the caller is not already running items in parallel, the m terms
+ * Pack(v[k], pK, k) are computed by the host threads (each exactly as in the serial loop) and
+ * added into `out` one at a time; addition in Z_Q is exact, so the order of the terms does not
+ * change the sum. */
 void or_vector_pack(const u64* P, const u64* pack, const u64* v, int m, u64* out) {
   int N = (int)P[P_N]; u64 Q = P[P_Q];
-  u64* t = (u64*)malloc(sizeof(u64) * 2 * N);
   memset(out, 0, sizeof(u64) * 2 * N);
-  for (int k = 1; k <= m; k++) {
-    or_pack(P, pack, v + (size_t)(k - 1) * (N + 1), k, t);
-    poly_add(N, Q, out, t, out); poly_add(N, Q, out + N, t + N, out + N);
+  #pragma omp parallel if (m >= 16 && !omp_in_parallel())
+  {
+    u64* t = (u64*)malloc(sizeof(u64) * 2 * N);
+    #pragma omp for schedule(dynamic, 1)
+    for (int k = 1; k <= m; k++) {
+      or_pack(P, pack, v + (size_t)(k - 1) * (N + 1), k, t);
+      #pragma omp critical(or_vector_pack_sum)
+      { poly_add(N, Q, out, t, out); poly_add(N, Q, out + N, t + N, out + N); }
+    }
+    free(t);
   }
-  free(t);
 }
 /* Shift(ct, pK, d), d in [N-1] with readings F2 (extract N-d+i),
  * F3 (d = N/2 takes branch 1; branch2 selectable for the tie test) and G4. */

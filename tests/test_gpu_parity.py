@@ -5,13 +5,15 @@ byte equality (no tolerance).  Keys for the hot-path parity tests are generated
 by the ORACLE and imported into the device format (fdfb_key_import); the GPU
 keygen is checked separately against the oracle keygen.
 """
+import os
+
 import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
 
 import synth  # noqa: E402
-from oracle.oracle import Oracle  # noqa: E402
+from oracle.oracle import Oracle, num_threads  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -22,6 +24,22 @@ from paper_2109_02731_b200 import KEY_BPK, KEY_BRK, KEY_KSK, Context  # noqa: E4
 from paper_2109_02731_b200 import KEY_PACK  # noqa: E402
 
 DEV = torch.device("cuda", 0)
+
+# Oracle sample sizes of the full-size tests.  The oracle's cost is fixed per item (schoolbook
+# products: ~400 core-seconds per Large bootstrap or per Config-4 Shift with m ~ N/2), so the
+# default sizes keep the whole `-m gpu` suite near 10 minutes on a 16-core host;
+# FDFB_PARITY_FULL=1 takes the larger samples (>= 16 Large bootstraps, every forced Shift item;
+# ~20 minutes; the log of such a run is kept under profiles/).
+FULL = os.environ.get("FDFB_PARITY_FULL") == "1"
+
+
+def per_item(fn, items, *args):
+    """Run an oracle batch function over `items`: one call when there are at least as many items
+    as host threads (the oracle parallelises over items), else one call per item (the oracle then
+    parallelises inside the item: rows of the ring product, terms of VectorPack).  Scheduling only."""
+    if len(items) >= num_threads():
+        return fn(items, *args)
+    return np.concatenate([fn(items[i:i + 1], *[a[i:i + 1] for a in args]) for i in range(len(items))])
 
 
 def T(a):
@@ -391,7 +409,8 @@ def test_shift_out_of_range_d_flagged():
 @pytest.mark.slow
 def test_bootstrap_large_full_batch_sampled_bit_exact():
     """Large configuration at the bench's batch (B = 4096: the ladder launch rotates B ell_boot =
-    20480 accumulators on 296 persistent CTAs, the final launch 4096): 16 outputs bit-exact with
+    20480 accumulators on 296 persistent CTAs, the final launch 4096): 8 outputs (16 with
+    FDFB_PARITY_FULL=1) bit-exact with
     the oracle -- a seeded random subsample plus items whose ladder accumulators fall in the
     last, partial wave of the ladder launch (accumulators >= 296 * 69, i.e. ciphertexts >= 4085)
     and in the last wave of the final launch.  The oracle computes them in parallel over the
@@ -406,8 +425,10 @@ def test_bootstrap_large_full_batch_sampled_bit_exact():
     rng = np.random.default_rng(202)
     tail = rng.choice(np.arange(4085, B), 3, replace=False)             # last ladder wave
     rest = rng.choice(np.setdiff1d(np.arange(B), tail), 13, replace=False)
+    if not FULL:
+        rest = rest[:5]                                                 # 8 items by default, 16 with FULL
     pick = np.sort(np.concatenate([tail, rest]))
-    ref = orc.bootstrap(K, rotp, cts[pick])
+    ref = per_item(lambda c: orc.bootstrap(K, rotp, c), cts[pick])
     for r, i in enumerate(pick):
         assert np.array_equal(got[i], ref[r]), int(i)
 
@@ -434,8 +455,9 @@ def test_bootstrap_large_full_batch_noiseless_full_domain():
 def test_shift_config4_full_batch():
     """Shift/VectorPack configuration at the bench's batch (1024 RLWE, d ~ U[1, 2047]) with the
     oracle's PackSetup key: three items forced to d = 1023, 1024 (= N/2, the tie -> branch 1)
-    and 1025 (branch 2), i.e. the largest packs m ~ N/2, plus two seeded random items, bit-exact
-    with the oracle; and every output decrypts to roll(m, d) within the lemma's bound."""
+    and 1025 (branch 2), i.e. the largest packs m ~ N/2, plus two seeded random items; of these
+    d = 1024, d = 1025 and one random item (all five with FDFB_PARITY_FULL=1) are compared
+    bit-exactly with the oracle; and every output decrypts to roll(m, d) within the lemma's bound."""
     cfg = synth.load_config("shift")
     orc = Oracle(cfg)
     s, S = orc.keygen_secrets(cfg["seeds"]["keys"])
@@ -450,15 +472,22 @@ def test_shift_config4_full_batch():
     ds[forced] = [N // 2 - 1, N // 2, N // 2 + 1]
     others = rng.choice(np.setdiff1d(np.arange(B), forced), 2, replace=False)
     cts = orc.rlwe_encrypt(cfg["seeds"]["err"], S, msg)
-    got = H(ctx.shift(dpk, T(cts), T(ds)))
+    d_cts = T(cts)
+    d_got = ctx.shift(dpk, d_cts, T(ds))
+    got = H(d_got)
     ctx.device_status()
-    pick = np.concatenate([forced, others])
-    ref = orc.shift_batch(pk, cts[pick], ds[pick])            # items in parallel on the host cores
+    # default: the tie d = N/2 (branch 1, m = N/2, the largest pack), d = N/2 + 1 (branch 2,
+    # m = N/2 - 1) and one random item; FULL adds d = N/2 - 1 and a second random item
+    pick = np.concatenate([forced, others]) if FULL else np.concatenate([forced[1:], others[:1]])
+    ref = per_item(lambda c, d: orc.shift_batch(pk, c, d), cts[pick], ds[pick])
     for r, i in enumerate(pick):
         assert np.array_equal(got[i], ref[r]), (int(i), int(ds[i]))
+    # every output decrypts to roll(m, d): phases by fdfb_rlwe_phase (itself checked against the
+    # oracle's phase at this ring in test_decryption_helpers_match_oracle[large]); the first four
+    # items also by a plain numpy phase, which must agree with it
     Qu = np.uint64(Q)
-    worst = 0
-    for c in range(B):
+    ph_all = H(ctx.rlwe_phase(T(S), d_got))
+    for c in range(4):
         ph = got[c, 0].copy()
         a = got[c, 1]
         for i in np.nonzero(S)[0]:
@@ -466,9 +495,11 @@ def test_shift_config4_full_batch():
             if S[i] < 0:
                 r = (Qu - r) % Qu
             ph = np.where(ph >= r, ph - r, ph + Qu - r)
-        e = (ph + Qu - np.roll(msg[c], int(ds[c]))) % Qu
-        e = np.minimum(e, Qu - e)
-        worst = max(worst, int(e.max()))
+        assert np.array_equal(ph, ph_all[c]), c
+    rolled = np.stack([np.roll(msg[c], int(ds[c])) for c in range(B)])
+    e = (ph_all + Qu - rolled) % Qu
+    e = np.minimum(e, Qu - e)
+    worst = int(e.max())
     assert worst < Q // 1024, worst
 
 

@@ -407,6 +407,25 @@ def test_shift_is_cyclic_rotation_all_d(toy_pack):
     assert np.array_equal(o.rlwe_phase(S, a), o.rlwe_phase(S, b))
 
 
+def test_vector_pack_schedule_changes_no_bytes(toy_cfg):
+    """The oracle adds the m terms Pack(v_k, pK, k) of VectorPack on the host
+    threads when it is called for one item, and serially per item inside a batch call: both give
+    the same bytes (the sum is exact in Z_Q), and they decrypt to the rotation (Lemma, 31-47)."""
+    cfg = dict(toy_cfg, N=64)                                  # 12289 = 1 mod 128; packs of m = 32 >= 16
+    o = Oracle(cfg, noiseless=True)
+    s, S = o.keygen_secrets(61)
+    pk = o.pack_key(62, S)
+    msg = np.random.default_rng(17).integers(0, o.Q, (3, o.N), dtype=np.uint64)
+    cts = o.rlwe_encrypt(63, S, msg)
+    ds = np.array([32, 33, 17], dtype=np.uint32)
+    batch = o.shift_batch(pk, cts, ds)                         # items in parallel, terms in order
+    for c in range(3):
+        one = o.shift_batch(pk, cts[c:c + 1], ds[c:c + 1])[0]  # one item: terms in parallel
+        assert np.array_equal(one, batch[c]), c
+        assert np.array_equal(one, o.shift(pk, cts[c], int(ds[c])))
+        assert np.array_equal(o.rlwe_phase(S, one), np.roll(msg[c], int(ds[c])))
+
+
 def test_shift_l2_error_bound_noisy(toy_cfg):
     """G15 / F9: ||e_out||_2 <= ||e_ct||_2 + N^2 ell max||e_pK||_2, checked per instance."""
     o = Oracle(toy_cfg)
