@@ -68,7 +68,9 @@ def parse():
     """CLI; --workload shift times fdfb_shift on the Shift/VectorPack configuration."""
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 3; 300 for --workload shift, whose step is ~10 ms, so that the "
+                         "timed region spans seconds and the clock sampler sees it)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fdfb", choices=["fdfb", "reference"])
     ap.add_argument("--config", default=None, help="configs/<name>.json (default: large / shift)")
@@ -83,6 +85,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPU box); gloo only for functional tests")
     a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 300 if (a.workload == "shift" and a.impl != "reference") else 3
     if a.config is None:
         a.config = "shift" if a.workload in ("shift", "permute", "shiftboot") else "large"
     return a

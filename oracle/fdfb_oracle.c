@@ -341,13 +341,18 @@ void or_ext_prod(int N, u64 Q, int logL, int ell, const u64* C, const u64* d, u6
       or_decomp(d[half * N + c], logL, ell, dig);
       for (int r = 0; r < ell; r++) D[((size_t)half * ell + r) * N + c] = dig[r];
     }
-  u64* prod = (u64*)malloc(sizeof(u64) * N);
+  /* Schedule only: the 2 ell x 2 ring products are independent, so a call that is not already
+   * inside a parallel region computes them on the host threads (each by the same or_ring_mul,
+   * which then runs its rows serially); they are added in the row order of the definition. */
+  u64* prod = (u64*)malloc(sizeof(u64) * (size_t)2 * ell * 2 * N);
   memset(out, 0, sizeof(u64) * 2 * N);
+  #pragma omp parallel for collapse(2) schedule(static) if (N >= 1024 && !omp_in_parallel())
   for (int row = 0; row < 2 * ell; row++)
-    for (int col = 0; col < 2; col++) {
-      or_ring_mul(N, Q, D + (size_t)row * N, C + ((size_t)row * 2 + col) * N, prod);
-      poly_add(N, Q, out + col * N, prod, out + col * N);
-    }
+    for (int col = 0; col < 2; col++)
+      or_ring_mul(N, Q, D + (size_t)row * N, C + ((size_t)row * 2 + col) * N, prod + ((size_t)row * 2 + col) * N);
+  for (int row = 0; row < 2 * ell; row++)
+    for (int col = 0; col < 2; col++)
+      poly_add(N, Q, out + col * N, prod + ((size_t)row * 2 + col) * N, out + col * N);
   free(prod); free(D); free(dig);
 }
 void or_cmux(int N, u64 Q, int logL, int ell, const u64* C, const u64* g, const u64* h, u64* out) {

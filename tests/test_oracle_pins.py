@@ -487,6 +487,48 @@ def _err(o, S, ct, msg):
     return [centered(int(p) - int(m), o.Q) for p, m in zip(o.rlwe_phase(S, ct), msg)]
 
 
+def test_ext_prod_schedule_changes_no_bytes():
+    """At N >= 1024 a single extProd call computes its 2 ell x 2 ring products on the host threads
+    and adds them in the definition's row order; inside a batch call the same
+    products run one after the other.  Pinned against the definition recomposed here from the
+    separately pinned primitives: sum_r Decomp(d)_r * C[r] with schoolbook products (library
+    routine: Python integers), on small-support operands so that big-int products stay cheap."""
+    import synth
+    cfg = synth.load_config("fhew")
+    o = Oracle(cfg)
+    N, Q, ell, logL = o.N, o.Q, o.ell["rgsw"], cfg["logL_rgsw"]
+    rng = np.random.default_rng(23)
+    Cm = np.zeros((2 * ell, 2, N), dtype=np.uint64)
+    sup = rng.choice(N, 6, replace=False)                      # sparse key rows: 6 non-zero coefficients each
+    Cm[:, :, sup] = rng.integers(0, Q, (2 * ell, 2, 6), dtype=np.uint64)
+    d = rng.integers(0, Q, (2, N), dtype=np.uint64)
+    got = o.ext_prod(Cm, d)                                    # one call: products in parallel
+    exp = [[0] * N for _ in range(2)]
+    for half in range(2):
+        digs = np.array([o.decomp(int(x), logL, ell) for x in d[half]], dtype=object)   # [N][ell]
+        for r in range(ell):
+            row = half * ell + r
+            for col in range(2):
+                for j in sup:                                  # (digit poly) * (sparse row), X^N = -1
+                    c = int(Cm[row, col, j])
+                    for i in range(N):
+                        k = i + int(j)
+                        v = int(digs[i][r]) * c
+                        if k >= N:
+                            exp[col][k - N] -= v
+                        else:
+                            exp[col][k] += v
+    assert [[int(x) for x in got[c]] for c in range(2)] == [[v % Q for v in exp[c]] for c in range(2)]
+    # and the serial schedule (calls made inside the oracle's parallel region over items) gives
+    # the same bytes as the per-item calls: one blind rotation each (TFHE bootstrap, 512 CMux)
+    K = o.keys(cfg["seeds"]["keys"])
+    rotp = o.setup_polynomial(o.bootsmap(synth.lut(cfg)))
+    cts = o.lwe_encrypt(5, K["s"], synth.messages(cfg, 2))
+    both = o.bootstrap_tfhe(K, rotp[0], cts)
+    for c in range(2):
+        assert np.array_equal(o.bootstrap_tfhe(K, rotp[0], cts[c:c + 1])[0], both[c]), c
+
+
 def test_cmux_error_variance_bound(toy_cfg):
     """Lemma CMux: B <= (1/3)(n+1) N ell L^2 B_C + max(B_g, B_h), n = 1."""
     o = Oracle(toy_cfg)
