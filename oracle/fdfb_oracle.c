@@ -16,7 +16,11 @@
  *     arithmetic is exact via unsigned __int128;
  *   - indices in comments are the paper's 1-based ones, arrays are 0-based;
  *   - where the paper is garbled the DESIGN.md reading (R1, F1..F6, G*) is
- *     named at the line that depends on it.
+ *     named at the line that depends on it;
+ *   - OpenMP is scheduling only: over independent items of a batch, and -- for a
+ *     call that carries one item -- over the rows of a ring product, the 2 ell x 2
+ *     independent ring products of an extProd (added in the definition's order)
+ *     and the m terms of a VectorPack (an exact, order-free sum in Z_Q).
  *
  * Canonical layouts (shared *format*, not code):
  *   LWE  = [b, a_1..a_n]             ([b, a^T]^T)
