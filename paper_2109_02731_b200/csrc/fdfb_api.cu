@@ -681,6 +681,7 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   CK(cudaMalloc(&c->d_prog, (size_t)BR_PACE_SLOTS * BR_PACE_MAXGRID * sizeof(u64)));
   CK(cudaMemset(c->d_prog, 0, (size_t)BR_PACE_SLOTS * BR_PACE_MAXGRID * sizeof(u64)));
   if (const char* e = getenv("FDFB_BR_PACE_SPLIT")) c->br_pace_split = atoi(e) != 0;
+  const bool pace_env = getenv("FDFB_BR_PACE") != nullptr;
   if (const char* e = getenv("FDFB_BR_PACE")) {
     unsigned lo = 0, hi = 0, cap = 0;
     const int nf = sscanf(e, "%u,%u,%u", &lo, &hi, &cap);
@@ -689,6 +690,15 @@ extern "C" int fdfb_ctx_create(const fdfb_params* p, int device, fdfb_ctx** out)
   }
   CK(cudaMemcpy(c->d_tables, h.data(), ntab * sizeof(u64), cudaMemcpyHostToDevice));
   if ((rc = setup_rns(c))) { delete c; return rc; }
+  if (!pace_env) {
+    // pacing keeps the brK reads of drifting CTAs in L2; a key that stays in L2 as a whole needs none,
+    // and the checks then only cost time (FHEW-like, 67 MB of brK: 173 -> 158 ms per 10 rounds unpaced,
+    // profiles/r02/fhewexp).  Paced by default only when the device-format brK exceeds 3/4 of L2.
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    const size_t brk_dev = (size_t)p->n * (p->lwe_key ? 2 : 1) * 2 * p->ell_rgsw * 2 * p->N * c->rns.np * sizeof(u32);
+    if (l2 > 0 && brk_dev <= (size_t)l2 / 4 * 3) c->br_wlo = c->br_whi = 0;
+  }
   if (const char* e = getenv("FDFB_BR_CLUSTER")) c->br_cluster = atoi(e);
   if (const char* e = getenv("FDFB_IMMA_CG")) c->imma_cg = atoi(e) == 1 ? 1 : 2;
   if (const char* e = getenv("FDFB_BR_KERNEL")) c->br_kernel = atoi(e) == 1 ? 1 : 2;
